@@ -1,0 +1,177 @@
+"""Seeded synthetic workloads shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds the five BASELINE.json configurations and
+the seeded generators of their *problem data*: grid coordinates, initial
+fields, the sampled source term and random apply inputs.  It deliberately holds
+none of the method's arithmetic: no spatial operator, no time-stepping matrix,
+no right-hand-side assembly, no DFT, no solve.  Both the oracle (``oracle/``)
+and the CUDA path (``paper_2005_09158_b200``) build everything else from these
+arrays on their own.
+
+Readings of the paper/BASELINE that fix the data:
+  c8  T=1 for configs 3/4 (dt = 1/Nt).
+  c9  "N(0,1e-3)" noise = standard deviation 1e-3, numpy PCG64 seeded.
+  c10 Gaussian bump exp(-(x-c)^2 / (2*0.05^2)), c ~ U(0.3, 0.7).
+  c11 config-1 source: sum_{k=1..8} a_k sin(k pi x) cos(t), a_k ~ N(0,1).
+  c12 configs 3/4: sum_{0<|k|<=8} (a_k cos(k.x) + b_k sin(k.x)) / |k|^2.
+  c13 1D Dirichlet grids hold interior nodes x_i=(i+1)h, h=1/(Nx+1);
+      periodic grids have no duplicate endpoint, x_i = i h, h = 2 pi / N.
+No public dataset is involved: the paper's workloads are analytic PDE data.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+# operator ids (mirror include/paradiag.h pd_operator)
+ADE1D = "ade1d"      # u_t = nu u_xx - a u_x on (0,1), homogeneous Dirichlet
+WAVE1D = "wave1d"    # u_tt = u_xx on (0,1), homogeneous Dirichlet
+ADE2D = "ade2d"      # u_t = nu Lap u - a.grad u on [0,2pi)^2, periodic
+
+# scheme ids (mirror pd_scheme)
+BE, CN, LF = "be", "cn", "lf"
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    """One all-at-once problem: grid, operator coefficients, time grid, alpha, solver."""
+    name: str
+    op: str
+    nx: int               # 1D: interior nodes; 2D: N per dimension
+    ny: int               # 1 for 1D; N for 2D
+    nt: int
+    T: float
+    scheme: str
+    alpha: float
+    nu: float = 1.0
+    ax: float = 0.0
+    ay: float = 0.0
+    solver: str = "stationary"   # "stationary" | "gmres"
+    tol: float = 1e-10
+    m: int = 20                  # GMRES restart length
+    maxit: int = 100
+    seed: int = 0
+    source: str = "zero"         # "zero" | "sin8cos"
+    init: str = "sin_noise"      # "sin_noise" | "bump" | "fourier8" | "exact_wave"
+
+    @property
+    def dt(self) -> float:
+        return self.T / self.nt
+
+    @property
+    def length(self) -> float:
+        return 1.0 if self.op in (ADE1D, WAVE1D) else 2.0 * math.pi
+
+    @property
+    def h(self) -> float:
+        if self.op in (ADE1D, WAVE1D):
+            return 1.0 / (self.nx + 1)
+        return 2.0 * math.pi / self.nx
+
+    @property
+    def S(self) -> int:
+        """Spatial dofs per time level."""
+        return self.nx * self.ny
+
+    @property
+    def D(self) -> int:
+        """All-at-once dofs Nt*Nx (the metric's unit of work)."""
+        return self.nt * self.S
+
+    def scaled(self, **kw) -> "Config":
+        return dataclasses.replace(self, **kw)
+
+
+# SURVEY.md §8(d) table; BASELINE.json "configs"
+CONFIGS = [
+    Config("cfg0", ADE1D, nx=63, ny=1, nt=32, T=1.0, scheme=BE, alpha=1e-2, nu=1e-2, ax=1.0,
+           solver="stationary", tol=1e-10, seed=0, init="sin_noise"),
+    Config("cfg1", ADE1D, nx=1023, ny=1, nt=1024, T=1.0, scheme=CN, alpha=1e-3, nu=1e-2, ax=1.0,
+           solver="gmres", tol=1e-10, m=20, seed=1, init="sin_noise", source="sin8cos"),
+    Config("cfg2", WAVE1D, nx=4095, ny=1, nt=4096, T=2.0, scheme=LF, alpha=1e-2,
+           solver="stationary", tol=1e-9, seed=2, init="bump"),
+    Config("cfg3", ADE2D, nx=256, ny=256, nt=256, T=1.0, scheme=BE, alpha=1e-3, nu=1e-2, ax=1.0, ay=0.5,
+           solver="gmres", tol=1e-10, m=20, seed=3, init="fourier8"),
+    Config("cfg4", ADE2D, nx=512, ny=512, nt=2048, T=1.0, scheme=CN, alpha=1e-4, nu=1e-2, ax=1.0, ay=0.5,
+           solver="gmres", tol=1e-9, m=10, seed=4, init="fourier8"),
+]
+BY_NAME = {c.name: c for c in CONFIGS}
+
+
+def grid(cfg: Config):
+    """Node coordinates (reading c13). 1D: x[Nx]; 2D: (X, Y) each [N][N], x fastest."""
+    if cfg.op in (ADE1D, WAVE1D):
+        return (np.arange(cfg.nx, dtype=np.float64) + 1.0) * cfg.h
+    x = np.arange(cfg.nx, dtype=np.float64) * cfg.h
+    y = np.arange(cfg.ny, dtype=np.float64) * (2.0 * math.pi / cfg.ny)
+    Y, X = np.meshgrid(y, x, indexing="ij")
+    return X, Y
+
+
+def initial_u0(cfg: Config) -> np.ndarray:
+    """U_0 on the grid, flattened [S] (x fastest)."""
+    rng = np.random.Generator(np.random.PCG64(cfg.seed))
+    if cfg.init == "sin_noise":            # configs 0, 1 (reading c9)
+        x = grid(cfg)
+        return np.sin(math.pi * x) + 1e-3 * rng.standard_normal(cfg.nx)
+    if cfg.init == "bump":                 # config 2 (reading c10)
+        x = grid(cfg)
+        c = rng.uniform(0.3, 0.7)
+        return np.exp(-((x - c) ** 2) / (2.0 * 0.05 ** 2))
+    if cfg.init == "fourier8":             # configs 3, 4 (reading c12)
+        X, Y = grid(cfg)
+        u = np.zeros_like(X)
+        for kx in range(-8, 9):
+            for ky in range(-8, 9):
+                k2 = kx * kx + ky * ky
+                if k2 == 0 or k2 > 64:
+                    continue
+                a, b = rng.standard_normal(2)
+                ph = kx * X + ky * Y
+                u += (a * np.cos(ph) + b * np.sin(ph)) / k2
+        return u.reshape(-1)
+    if cfg.init == "exact_wave":           # u = sin(pi x) e^t (1D analogue of P:l.1311-1314)
+        x = grid(cfg)
+        return np.sin(math.pi * x)
+    raise ValueError(cfg.init)
+
+
+def initial_v0(cfg: Config) -> np.ndarray:
+    """u_t(0) for the wave problems ([S]); zeros elsewhere."""
+    if cfg.init == "exact_wave":
+        return np.sin(math.pi * grid(cfg))
+    return np.zeros(cfg.S)
+
+
+def source_samples(cfg: Config):
+    """f(x, t_n) sampled at t_n = n dt, n = 0..Nt, shape [Nt+1][S]; None when f = 0."""
+    if cfg.source == "zero":
+        return None
+    t = np.arange(cfg.nt + 1, dtype=np.float64) * cfg.dt
+    if cfg.source == "sin8cos":            # config 1 (reading c11)
+        rng = np.random.Generator(np.random.PCG64(1000 + cfg.seed))
+        a = rng.standard_normal(8)
+        x = grid(cfg)
+        shape = sum(a[k - 1] * np.sin(k * math.pi * x) for k in range(1, 9))
+        return np.cos(t)[:, None] * shape[None, :]
+    if cfg.source == "exact_wave":         # f = (1 + pi^2) sin(pi x) e^t for u = sin(pi x) e^t
+        x = grid(cfg)
+        return np.exp(t)[:, None] * ((1.0 + math.pi ** 2) * np.sin(math.pi * x))[None, :]
+    raise ValueError(cfg.source)
+
+
+def random_vector(cfg: Config, seed: int | None = None) -> np.ndarray:
+    """r ~ N(0,1) iid, shape [Nt][S] (seed 100 + cfg index)."""
+    if seed is None:
+        seed = 100 + (CONFIGS.index(BY_NAME[cfg.name]) if cfg.name in BY_NAME else 0)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.standard_normal((cfg.nt, cfg.S))
+
+
+def exact_wave_solution(cfg: Config) -> np.ndarray:
+    """sin(pi x) e^{t_n}, n = 1..Nt ([Nt][S]) for the second-order pin of reading c4."""
+    x = grid(cfg)
+    t = np.arange(1, cfg.nt + 1, dtype=np.float64) * cfg.dt
+    return np.exp(t)[:, None] * np.sin(math.pi * x)[None, :]
