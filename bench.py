@@ -1,0 +1,341 @@
+"""Benchmark of the ParaDiag-II hot path on B200 (see DESIGN.md §6 for the protocol).
+
+A step = one complete ParaDiag-II solve of the workload (all SURVEY §8(a) rows: residuals, Steps (a)-(c)
+of every P_alpha^{-1} apply, the Krylov / stationary update) on synthetic seeded data already resident
+in HBM.  value = all-at-once dofs (Nt*Nx, all ranks) solved per second.  The apply throughput
+(applies/s, apply dofs/s, % of HBM roofline under the 48 B/dof model) is reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "P_alpha^{-1} applies/s and solve time (Nt*Nx dofs/s, % HBM roofline) at 1/2/4/8 GPU"
+FALLBACK_HBM = 6650.0
+PHASES = ["tfft_fwd", "spatial_solve", "tfft_inv", "residual", "tfft_inv_update", "matvec"]
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def phase_bytes(cfg, S_local):
+    """Algorithmic HBM bytes per launch of each timed kernel."""
+    D = cfg.nt * S_local
+    spec = (cfg.nt // 2 + 1) * S_local * 16
+    return {0: D * 8 + spec, 1: 2 * spec, 2: spec + D * 8, 3: 3 * D * 8, 4: spec + 2 * D * 8, 5: 2 * D * 8}
+
+
+def oracle_sample_cfg(cfg):
+    """Bounded sample of the workload for the CPU oracle (~10-30 s of CPU work): same recipe, fewer dofs."""
+    if cfg.op == W.ADE2D:
+        return cfg.scaled(nx=min(cfg.nx, 128), ny=min(cfg.ny, 128), nt=min(cfg.nt, 512))
+    return cfg.scaled(nx=min(cfg.nx, 1023), nt=min(cfg.nt, 1024))
+
+
+def run_oracle_solve(cfg):
+    from oracle import problems, solvers
+    b = problems.rhs(cfg, W.initial_u0(cfg), W.initial_v0(cfg), W.source_samples(cfg))
+    t0 = time.perf_counter()
+    if cfg.solver == "stationary":
+        _, rep = solvers.solve_stationary(cfg, b)
+    else:
+        _, rep = solvers.solve_gmres(cfg, b)
+    return time.perf_counter() - t0, rep
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 0) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg):
+    s = oracle_sample_cfg(cfg)
+    sec, rep = run_oracle_solve(s)
+    return {"value": s.D / sec, "unit": "dofs/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{cfg.name} recipe at Nx={s.nx}x{s.ny}, Nt={s.nt} ({s.D} dofs): one oracle O1 "
+                      f"{s.solver} solve ({rep.iterations} its) in {sec:.2f} s on the host cores"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md recipe)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--apply-reps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = W.BY_NAME[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2005_09158_b200 import ParaDiag, nccl_unique_id
+    from tests.helpers import ctor_args
+
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    ctx = ParaDiag(**ctor_args(cfg), stream=stream, rank=rank, size=world, nccl_id=nccl_id)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    # ---- inputs resident in HBM: initial data -> b on device (pd_build_rhs) ----
+    u0 = W.initial_u0(cfg)
+    v0 = W.initial_v0(cfg)
+    f = W.source_samples(cfg)
+    sl = slice(ctx.offset, ctx.offset + ctx.S)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    b = ctx.build_rhs(dev(u0[sl]), dev(v0[sl]) if cfg.op == W.WAVE1D else None,
+                      None if f is None else dev(np.ascontiguousarray(f[:, sl])))
+    u = torch.zeros_like(b)
+
+    def step():
+        u.zero_()
+        if cfg.solver == "stationary":
+            return ctx.solve_stationary(b, u, tol=cfg.tol, maxit=cfg.maxit)[1]
+        return ctx.solve_gmres(b, u, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)[1]
+
+    for _ in range(args.warmup):
+        rep = step()
+    barrier()
+    launches0 = ctx.kernel_launches()
+    ctx.enable_phase_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        its = []
+        for _ in range(args.steps):
+            rep = step()
+            its.append(rep.iterations)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.kernel_launches() - launches0
+    pms, pn = ctx.phase_times()
+    ctx.enable_phase_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cfg.D / (ms / 1e3)
+
+    # ---- apply throughput (same stream, inputs > L2) ----
+    r = torch.randn(ctx.shape, dtype=torch.float64, device="cuda")
+    z = torch.empty_like(r)
+    for _ in range(3):
+        ctx.apply_precond(r, z)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.apply_reps):
+        ctx.apply_precond(r, z)
+    e1.record(stream)
+    barrier()
+    ams = e0.elapsed_time(e1) / args.apply_reps
+    if world > 1:
+        t = torch.tensor([ams], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ams = float(t.item())
+    del r, z
+    peak, peak_src = hbm_peak()
+    apply_gbs = 48.0 * cfg.D / (ams / 1e3) / 1e9
+
+    # ---- dominant kernel roofline ----
+    pb = phase_bytes(cfg, ctx.S)
+    dom = max(range(6), key=lambda i: pms[i])
+    dom_ms = pms[dom] / max(pn[dom], 1)
+    achieved = pb[dom] / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as fh:
+                traffic = json.load(fh).get(cfg.name, {}).get(PHASES[dom])
+        except Exception:
+            traffic = None
+    phases = {PHASES[i]: {"ms_per_launch": round(pms[i] / pn[i], 4), "launches": int(pn[i]),
+                          "share": round(pms[i] / max(sum(pms), 1e-30), 4),
+                          "GBps": round(pb[i] / (pms[i] / pn[i] / 1e3) / 1e9, 1)}
+              for i in range(6) if pn[i]}
+
+    # ---- end to end through the host-buffer C ABI (pinned host b, u; H2D + solve + D2H per step) ----
+    e2e = None
+    if not args.no_e2e:
+        bh = b.cpu().pin_memory()
+        uh = torch.zeros_like(bh).pin_memory()
+        solver = 0 if cfg.solver == "stationary" else 1
+
+        def step_e2e():
+            uh.zero_()
+            ctx.solve_host(solver, bh, uh, cfg.tol, cfg.m, cfg.maxit)
+
+        step_e2e()
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        ksteps = max(1, min(args.steps, 3))
+        for _ in range(ksteps):
+            step_e2e()
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1) / ksteps
+        wall = (time.perf_counter() - t0) * 1e3 / ksteps
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        nb = bh.numel() * 8
+        e2e = {"value": cfg.D / (ems / 1e3), "unit": "dofs/s", "h2d_bytes_per_step": 2 * nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": round(ems, 3), "wall_ms_per_step": round(wall, 3)}
+        del bh, uh
+
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+    out = {
+        "metric": METRIC, "value": value, "unit": "dofs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "op": cfg.op, "nx": cfg.nx, "ny": cfg.ny, "nt": cfg.nt,
+                   "scheme": cfg.scheme, "alpha": cfg.alpha, "solver": f"{cfg.solver}" + (
+                       f"({cfg.m})" if cfg.solver == "gmres" else ""), "tol": cfg.tol, "dofs": cfg.D,
+                   "iterations": its[-1], "l2": "inputs larger than L2 (vectors %.2f GB > 126 MB)" % (cfg.D * 8 / 1e9)
+                   if cfg.D * 8 > 126e6 else "working set fits L2 (no flush); latency regime",
+                   "parallelism": f"space/frequency transpose x{world}" if world > 1 else "1 GPU"},
+        "apply": {"ms": round(ams, 4), "applies_per_s": 1e3 / ams, "dofs_per_s": cfg.D / (ams / 1e3),
+                  "hbm_GBps_48B_model": round(apply_gbs, 1), "hbm_frac": round(apply_gbs / peak, 4)},
+        "roofline": {"bound": "hbm", "kernel": PHASES[dom], "achieved": round(achieved, 1), "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "alg_bytes_per_launch": pb[dom], "ms_per_launch": round(dom_ms, 4)},
+        "phases": phases,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "cpu_baseline": cpu,
+    }
+    clk_s = clk.summary()
+    if clk_s:
+        out["clocks"] = clk_s
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, rank, world):
+    """The oracle arm: the CPU oracle as it stands, on bounded samples of the same workload."""
+    if rank != 0:
+        return
+    s = oracle_sample_cfg(cfg)
+    for _ in range(args.warmup):
+        run_oracle_solve(s)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sec, rep = run_oracle_solve(s)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    value = s.D / (ms / 1e3)
+    cores = blas_threads()
+    out = {"metric": METRIC, "value": value, "unit": "dofs/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": cfg.name, "sample": f"Nx={s.nx}x{s.ny}, Nt={s.nt}", "dofs": s.D,
+                      "solver": cfg.solver, "iterations": rep.iterations},
+           "cpu_baseline": {"value": value, "unit": "dofs/s", "cores": cores, "kind": "oracle",
+                            "sample": f"{cfg.name} recipe at {s.D} dofs (Nx={s.nx}x{s.ny}, Nt={s.nt}), oracle O1 "
+                                      f"{cfg.solver} solve per step"},
+           "e2e": {"value": value, "unit": "dofs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * paradiag.h — C ABI of the B200 ParaDiag-II hot path (arXiv 2005.09158).
+ *
+ * What it computes (P:l.N = /root/reference/PAPER.md line N):
+ *   all-at-once system      A = B1 (x) M + B2 (x) K              (P:l.80-84, eq 1.1), M = I (P:l.74-76)
+ *   preconditioner          P_alpha = C1 (x) M + C2 (x) K         (P:l.114-116, eq 1.2; corners eq 2.11b, 3.4)
+ *   apply z = P_alpha^{-1} r in three steps                       (P:l.179-185 eq 1.3; P:l.813-819 eq 2.12)
+ *     (a) S1 = (F (x) I)(Gamma_alpha (x) I) r       time FFT of every spatial dof, Gamma fused
+ *     (b) S2_n = (lambda_{1,n} I + lambda_{2,n} K)^{-1} S1_n     batched complex-shifted spatial solves
+ *     (c) z = (Gamma_alpha^{-1} (x) I)(F^* (x) I) S2             inverse time FFT, Gamma^{-1} fused
+ *   residual r = b - A u                                          (P:l.1563-1565, eq 5.1)
+ *   stationary iteration u <- u + P_alpha^{-1}(b - A u)           (P:l.120-124, eq 5.1)
+ *   right-preconditioned GMRES(m) on A P_alpha^{-1}               (P:l.125-132; stop rule P:l.1315-1317)
+ *
+ * Vectors.  Unless a function says HOST, every vector argument is a DEVICE pointer to fp64 data owned
+ * by the caller, laid out time-major: 1D [Nt][Nx], 2D [Nt][Ny][Nx] with x fastest; block n holds time
+ * level t_{n+1} = (n+1) dt (U_1 .. U_Nt of eq 1.1).  Work is enqueued on the context's CUDA stream
+ * (pd_setup argument); calls return once the work is enqueued unless stated otherwise.
+ *
+ * Errors.  Every entry point returns a pd_status and never aborts or throws across the ABI.
+ * pd_last_error() returns a description of the last failure on that context (or of the last failed
+ * pd_setup when given NULL).
+ *
+ * Threading.  One context per (device, stream); a context is not reentrant.
+ */
+#ifndef PARADIAG_H
+#define PARADIAG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define PD_API __attribute__((visibility("default")))
+#else
+#define PD_API
+#endif
+
+typedef struct pd_ctx pd_ctx; /* opaque: owns workspace, tables, streams, NCCL communicator */
+
+typedef enum {
+  PD_OK = 0,
+  PD_NOT_CONVERGED = 1, /* non-fatal: maxit exhausted, report filled, last iterate in u */
+  PD_EINVAL = -1,       /* bad argument (alpha outside (0,1], Nt not a power of two, ...) */
+  PD_ESINGULAR = -2,    /* a shifted system lambda_1 I + lambda_2 K is singular (message names n) */
+  PD_ECUDA = -3,        /* a CUDA runtime error (message holds cudaGetErrorString) */
+  PD_ENCCL = -4,        /* an NCCL error (multi-GPU) */
+  PD_ENOMEM = -5,       /* device allocation failed */
+  PD_EBREAKDOWN = -6    /* GMRES breakdown above tolerance */
+} pd_status;
+
+typedef enum { PD_BE = 0, PD_CN = 1, PD_LEAPFROG = 2 } pd_scheme;
+
+typedef enum {
+  PD_ADE1D_DIRICHLET = 0,  /* u_t = nu u_xx - ax u_x on (0,L), u=0 at both ends, Nx interior nodes, h = L/(Nx+1) */
+  PD_WAVE1D_DIRICHLET = 1, /* u_tt = nu u_xx on (0,L), Dirichlet (nu = c^2; use PD_LEAPFROG)                  */
+  PD_ADE2D_PERIODIC = 2    /* u_t = nu Lap u - (ax, ay).grad u on [0,L)^2 periodic, N x N, h = L/N (5-point)  */
+} pd_operator;
+
+typedef struct {
+  pd_operator op;
+  int nx, ny;       /* 1D: nx = Nx, ny = 1.  2D: nx = ny = N (power of two) */
+  double length;    /* domain length L (1 for the 1D configs, 2*pi for the 2D configs) */
+  double nu, ax, ay;
+} pd_grid;
+
+typedef struct {
+  int rank, size;               /* size == 1 => single GPU (nccl_id ignored) */
+  const void* nccl_id;          /* 128-byte ncclUniqueId shared by all ranks (from pd_nccl_unique_id) */
+} pd_dist;
+
+typedef struct {
+  int iterations;       /* P_alpha^{-1} applications inside the loop (GMRES final assembly not counted) */
+  int converged;        /* 1 if ||b - A u|| <= tol ||b|| at exit */
+  double rel_residual;  /* true ||b - A u||_2 / ||b||_2 at exit */
+  double wall_ms;       /* host wall time of the call */
+  double* history;      /* HOST, caller-owned, capacity history_cap (may be NULL): per-iteration relative
+                           residuals (true residual for stationary, Arnoldi estimate for GMRES) */
+  int history_cap;
+  int history_len;
+} pd_report;
+
+/* Create a context: validate, build the spectra lambda_{1,n}, lambda_{2,n} (Lemma 1, P:l.155-174; closed
+ * forms DESIGN.md §3), Gamma tables, twiddles; allocate the workspace; check every shifted system for
+ * singularity.  alpha in (0,1]; Nt a power of two (>= 2, >= 4 for PD_LEAPFROG); dt > 0.
+ * cuda_stream: a cudaStream_t (NULL = legacy default stream).  dist may be NULL (single GPU).
+ * Returns PD_EINVAL / PD_ESINGULAR / PD_ENOMEM / PD_ECUDA / PD_ENCCL on failure (*out = NULL). */
+PD_API pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme s, const pd_dist* dist,
+                   void* cuda_stream, pd_ctx** out);
+PD_API void pd_destroy(pd_ctx* ctx);
+PD_API const char* pd_last_error(const pd_ctx* ctx);
+
+/* The 128-byte NCCL unique id for a multi-GPU setup (rank 0 creates it and broadcasts it). */
+PD_API pd_status pd_nccl_unique_id(void* out128);
+
+/* Local slab of this rank: 1D x-range [offset, offset+nx_local), 2D y-rows [offset/nx, ...). */
+PD_API pd_status pd_local_shape(const pd_ctx* ctx, int* nx_local, int* ny_local, long long* offset);
+/* Elements of one local all-at-once vector (Nt * local spatial dofs). */
+PD_API long long pd_local_size(const pd_ctx* ctx);
+
+/* Copy the spectra (numpy convention, n = 0..Nt-1) to HOST arrays lam1[2*Nt], lam2[2*Nt] (re, im). */
+PD_API pd_status pd_spectra(const pd_ctx* ctx, double* lam1_host, double* lam2_host);
+
+/* z = P_alpha^{-1} r (Steps (a)-(c)).  r, z: device [Nt][local spatial dofs]; r == z allowed. */
+PD_API pd_status pd_apply_precond(pd_ctx* ctx, const double* r, double* z);
+
+/* r = b - A u (all three device vectors; r may alias neither b nor u).  If rnorm2_host != NULL the call
+ * synchronises the stream and stores ||r||_2^2 (deterministic fixed-order reduction). */
+PD_API pd_status pd_residual(pd_ctx* ctx, const double* b, const double* u, double* r, double* rnorm2_host);
+/* w = A u. */
+PD_API pd_status pd_matvec(pd_ctx* ctx, const double* u, double* w);
+
+/* b of A u = b from the initial data and the source (DESIGN.md §3 readings c4, c5):
+ *   u0, v0: device [local spatial dofs] (v0 may be NULL = 0; used by PD_LEAPFROG only)
+ *   f: device [(Nt+1)][local spatial dofs] sampled at t_n = n dt, n = 0..Nt, or NULL for f = 0. */
+PD_API pd_status pd_build_rhs(pd_ctx* ctx, const double* u0, const double* v0, const double* f, double* b);
+
+/* Stationary ParaDiag-II iteration (eq 5.1) from the initial guess in u until ||b-Au|| <= tol ||b||. */
+PD_API pd_status pd_solve_stationary(pd_ctx* ctx, const double* b, double* u, double tol, int maxit, pd_report* rep);
+/* Right-preconditioned restarted GMRES(m), CGS2 orthogonalisation, deterministic reductions.
+ * Workspace for the basis ((m+1) vectors) is allocated on first use and kept by the context. */
+PD_API pd_status pd_solve_gmres(pd_ctx* ctx, const double* b, double* u, double tol, int m, int maxit, pd_report* rep);
+
+/* HOST-buffer variants for end-to-end use: copy the HOST input(s) to device workspace on the context
+ * stream (pinned memory recommended), run, copy the HOST output back, synchronise. */
+PD_API pd_status pd_apply_precond_host(pd_ctx* ctx, const double* r_host, double* z_host);
+PD_API pd_status pd_solve_host(pd_ctx* ctx, int solver /*0 stationary, 1 gmres*/, const double* b_host,
+                        double* u_host, double tol, int m, int maxit, pd_report* rep);
+
+/* Number of kernels this context has launched so far (for the bench's gpu_launches claim). */
+PD_API long long pd_kernel_launches(const pd_ctx* ctx);
+
+/* Per-kernel timing: when enabled, the library records CUDA events on the context stream around every
+ * kernel of the path, without host synchronisation, and pd_phase_times (which synchronises) returns the
+ * accumulated device milliseconds and launch counts per slot:
+ *   0 Step (a) time FFT, 1 Step (b) spatial solve, 2 Step (c) inverse time FFT, 3 residual b - A u,
+ *   4 Step (c) fused with the update u += z, 5 matvec A u, 6-7 reserved.   ms8, count8: HOST arrays of 8. */
+PD_API pd_status pd_enable_phase_timing(pd_ctx* ctx, int enable);
+PD_API pd_status pd_phase_times(pd_ctx* ctx, double* ms8, long long* count8);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARADIAG_H */

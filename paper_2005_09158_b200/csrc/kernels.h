@@ -1,0 +1,70 @@
+// Internal launcher prototypes of the ParaDiag-II CUDA kernels (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+// ---- Steps (a)/(c): time-axis FFTs (tfft.cu) ----
+int pd_tfft_supported(int nt);
+cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+                               const double2* tw, cudaStream_t st);
+cudaError_t pd_launch_tfft_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+                               const double2* tw, int accumulate, cudaStream_t st);
+
+// ---- Step (b), 1D: batched constant-coefficient complex tridiagonal solves (tridiag.cu) ----
+// Per frequency n (row n of Sh, nx entries): (a_n x_{i-1} + b_n x_i + c_n x_{i+1}) = d_i with
+// a_n = lam2_n*sub, b_n = lam1_n + lam2_n*dia, c_n = lam2_n*sup.  coef[n] holds the host-computed
+// per-frequency constants (see struct below).
+struct pd_tri_coef {
+  double2 r2;    // characteristic root with |r2| <= |r1| of c r^2 + b r + a = 0  (= a tau)
+  double2 s;     // 1/r1 (= c tau)
+  double2 tau;   // 1/(c r1) = 2/(-b -+ sqrt(b^2 - 4ac)), larger-magnitude denominator
+  double2 c;     // super-diagonal c = lam2 * sup
+  double2 r2L;   // r2^L (L = rows per thread)
+  double2 sL;    // s^L
+};
+cudaError_t pd_launch_tridiag(double2* Sh, int nx, int nfreq, const pd_tri_coef* coef, int rows_per_thread,
+                              cudaStream_t st);
+int pd_tridiag_rows_per_thread();
+int pd_tridiag_threads(int nx);
+
+// ---- Step (b), 2D periodic: per-frequency slab 2D FFT -> divide -> inverse 2D FFT (slab2d.cu) ----
+// denominators lambda1_n + lambda2_n kappa(kx, ky), kappa = kd*(sx[kx]+sx[ky]) + i*(ax sn[kx] + ay sn[ky])/h
+struct pd_slab_params {
+  double kd;     // 4 nu / h^2
+  double cx, cy; // ax / h, ay / h
+};
+int pd_slab2d_supported(int n);
+cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
+                             const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
+                             int num_clusters, int cluster_size, cudaStream_t st);
+int pd_slab2d_max_clusters(int n, int cluster_size);
+
+// ---- all-at-once residual / matvec (stencil.cu) ----
+struct pd_stencil {
+  int op;            // 0 ADE1D, 1 WAVE1D, 2 ADE2D
+  int scheme;        // 0 BE, 1 CN, 2 LF
+  int nx, ny, nt;    // local sizes (2D: nx = N columns, ny = rows)
+  double sub, dia, sup;          // 1D K stencil
+  double k2c, k2x_m, k2x_p, k2y_m, k2y_p;  // 2D K stencil: centre, x-1, x+1, y-1, y+1
+  double dt;
+  double theta;
+};
+// out = b - A u (b != NULL) or out = A u (b == NULL); per-block partial sums of out^2 into partial[]
+cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double* u, double* out, double* partial,
+                              int* nblocks_out, cudaStream_t st);
+// b of A u = b from u0, v0 (nullable), f (nullable, [Nt+1][S])
+cudaError_t pd_launch_rhs(const pd_stencil& p, const double* u0, const double* v0, const double* f, double* b,
+                          cudaStream_t st);
+
+// ---- deterministic BLAS-1 (blas1.cu) ----
+int pd_blas_blocks();
+// partial[blk*k + i] = sum over block's range of x_i . y  (x_i = X[i], i < k)
+cudaError_t pd_launch_multidot(const double* const* X, int k, const double* y, long long n, double* partial,
+                               cudaStream_t st);
+// sum partials in fixed order: out[i] = sum_blk partial[blk*k + i]  (device out)
+cudaError_t pd_launch_reduce_partials(const double* partial, int nblk, int k, double* out, cudaStream_t st);
+// y = alpha*y + sum_i coef[i] * X[i]   (coef on device)
+cudaError_t pd_launch_multiaxpy(double* y, double alpha, const double* const* X, const double* coef, int k,
+                                long long n, cudaStream_t st);
+// y = a*x (+ y if accumulate)
+cudaError_t pd_launch_scale(double* y, const double* x, double a, long long n, cudaStream_t st);
+cudaError_t pd_launch_axpy(double* y, const double* x, double a, long long n, cudaStream_t st);

@@ -1,0 +1,851 @@
+// Host runtime and C ABI of the B200 ParaDiag-II hot path (see include/paradiag.h for the contract).
+//
+// pd_setup builds every data-independent quantity once (spectra from closed forms, Gamma tables,
+// twiddles, per-frequency tridiagonal constants, 2D symbol tables), checks the shifted systems for
+// singularity and allocates the workspace.  The solver loops (eq 5.1 stationary iteration, right-
+// preconditioned GMRES(m)) run on the host and enqueue the kernels of csrc/*.cu on the context stream.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/paradiag.h"
+#include "comm.h"
+#include "kernels.h"
+
+typedef std::complex<long double> cld;
+
+struct pd_ctx {
+  // problem
+  pd_grid g{};
+  double dt = 0, alpha = 0;
+  int nt = 0, F = 0;
+  pd_scheme scheme = PD_BE;
+  cudaStream_t st = nullptr;
+  // distribution
+  int rank = 0, size = 1;
+  pd_comm* comm = nullptr;
+  int nx_loc = 0, ny_loc = 0;    // local spatial extent (1D: x-range, 2D: y-rows)
+  long long off = 0;             // first local spatial dof (global index)
+  long long S = 0;               // local spatial dofs
+  long long Sg = 0;              // global spatial dofs
+  // tables (device)
+  double* gam = nullptr;
+  double* igam = nullptr;
+  double2* tw_t = nullptr;       // exp(-2 pi i j / Nt)
+  double2* lam1 = nullptr;       // half spectrum, F entries
+  double2* lam2 = nullptr;
+  pd_tri_coef* tri = nullptr;    // 1D
+  double* sx = nullptr;          // 2D: sin^2(pi k / N)
+  double* sn = nullptr;          // 2D: sin(2 pi k / N)
+  double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
+  pd_slab_params slab{};
+  int slab_clusters = 0, slab_cs = 0;
+  pd_stencil sten{};
+  // host copies
+  std::vector<std::complex<double>> lam1_full, lam2_full;
+  // workspace
+  double2* Sh = nullptr;         // half spectrum [F][S] complex (frequency-sharded layout when size > 1)
+  double* rvec = nullptr;        // residual / temp vector
+  double* partial = nullptr;     // reduction partials
+  int npartial = 0;
+  double* dred = nullptr;        // reduced scalars (device)
+  double* hred = nullptr;        // pinned host scalars
+  // GMRES
+  int gm_m = 0;
+  std::vector<double*> V;
+  double* zvec = nullptr;
+  // host-buffer staging
+  double* stage_a = nullptr;
+  double* stage_b = nullptr;
+  // diagnostics
+  long long launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> evpool;          // recorded pairs, resolved lazily (no sync per phase)
+  std::vector<std::pair<int, int>> evrec;   // (phase, index of begin event)
+  int ev_open[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  double phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long phase_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::string err;
+};
+
+static thread_local std::string g_setup_err;
+
+static pd_status fail(pd_ctx* c, pd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c)
+    c->err = buf;
+  else
+    g_setup_err = buf;
+  return s;
+}
+
+#define PD_CUDA(ctx, expr)                                                                    \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, PD_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define PD_LAUNCH(ctx, expr) \
+  do {                       \
+    PD_CUDA(ctx, expr);      \
+    (ctx)->launches++;       \
+  } while (0)
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc((void**)p, n * sizeof(T) + 16);
+}
+
+// ------------------------------------------------------------------------------------------------
+// spectra: closed forms of the DFT of the Gamma-weighted first columns (Lemma 1, P:l.155-174;
+// SURVEY §8(c) / DESIGN.md §3): z_n = alpha^{1/Nt} exp(-2 pi i n / Nt) (numpy convention, reading c1)
+//   BE: lam1 = (1 - z)/dt, lam2 = 1;  CN: lam1 = (1 - z)/dt, lam2 = (1 + z)/2
+//   LF: lam1 = (1 - z)^2/dt^2, lam2 = (1 + z^2)/2
+// ------------------------------------------------------------------------------------------------
+static void closed_form_spectra(int nt, double alpha, double dt, pd_scheme s, std::vector<cld>& l1,
+                                std::vector<cld>& l2) {
+  l1.resize(nt);
+  l2.resize(nt);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const long double a = powl((long double)alpha, 1.0L / nt);
+  for (int n = 0; n < nt; ++n) {
+    // exact argument reduction of n/Nt before the trig call
+    const long double th = 2.0L * pi * (long double)n / (long double)nt;
+    const cld z = a * cld(cosl(th), -sinl(th));
+    const long double d = dt;
+    if (s == PD_BE) {
+      l1[n] = (1.0L - z) / d;
+      l2[n] = 1.0L;
+    } else if (s == PD_CN) {
+      l1[n] = (1.0L - z) / d;
+      l2[n] = (1.0L + z) / 2.0L;
+    } else {
+      l1[n] = (1.0L - z) * (1.0L - z) / (d * d);
+      l2[n] = (1.0L + z * z) / 2.0L;
+    }
+  }
+}
+
+static inline double2 d2(cld v) { return make_double2((double)v.real(), (double)v.imag()); }
+
+// per-frequency constants of the Toeplitz tridiagonal recurrence solver (tridiag.cu)
+static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vector<cld>& l2, double sub, double dia,
+                           double sup, std::vector<pd_tri_coef>& out) {
+  const int N = c->g.nx, L = pd_tridiag_rows_per_thread();
+  out.resize(c->F);
+  for (int n = 0; n < c->F; ++n) {
+    const cld A = l2[n] * (long double)sub, B = l1[n] + l2[n] * (long double)dia, Cc = l2[n] * (long double)sup;
+    const cld D = std::sqrt(B * B - 4.0L * A * Cc);
+    cld den1 = -B - D, den2 = -B + D;
+    const cld den = std::abs(den1) >= std::abs(den2) ? den1 : den2;  // = 2 c r1 (larger root)
+    if (std::abs(den) == 0.0L) return fail(c, PD_ESINGULAR, "shifted system n=%d is singular (b = 0, ac = 0)", n);
+    const cld tau = 2.0L / den;
+    const cld r2 = A * tau, s = Cc * tau;
+    // stability of the two first-order recurrences over the N rows
+    const long double g2 = powl(std::abs(r2), (long double)N), gs = powl(std::abs(s), (long double)N);
+    if (!(g2 < 1e8L) || !(gs < 1e8L))
+      return fail(c, PD_EINVAL,
+                  "shifted system n=%d: characteristic roots |r2|=%.6Lf |1/r1|=%.6Lf outside the stable regime of "
+                  "the recurrence solver",
+                  n, std::abs(r2), std::abs(s));
+    // singularity: x_0 = x^(d)_0 / (1 - c q_0),  q_0 = -tau sum_{j<N} s^j r2^{j+1}
+    cld q0 = 0.0L, sp = 1.0L, rp = r2;
+    for (int j = 0; j < N; ++j) {
+      q0 += sp * rp;
+      sp *= s;
+      rp *= r2;
+    }
+    q0 *= -tau;
+    const cld piv = 1.0L - Cc * q0;
+    if (std::abs(piv) < 1e-12L)
+      return fail(c, PD_ESINGULAR, "shifted system lambda1 I + lambda2 K singular at frequency n=%d (|1-c q0|=%.3Le)",
+                  n, std::abs(piv));
+    pd_tri_coef t;
+    t.r2 = d2(r2);
+    t.s = d2(s);
+    t.tau = d2(tau);
+    t.c = d2(Cc);
+    cld r2L = 1.0L, sL = 1.0L;
+    for (int j = 0; j < L; ++j) {
+      r2L *= r2;
+      sL *= s;
+    }
+    t.r2L = d2(r2L);
+    t.sL = d2(sL);
+    out[n] = t;
+  }
+  return PD_OK;
+}
+
+static void free_ctx(pd_ctx* c) {
+  if (!c) return;
+  void* ptrs[] = {c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
+                  c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (double* p : c->V) cudaFree(p);
+  if (c->hred) cudaFreeHost(c->hred);
+  for (auto& e : c->evpool)
+    if (e) cudaEventDestroy(e);
+  if (c->comm) pd_comm_destroy(c->comm);
+  delete c;
+}
+
+extern "C" {
+
+const char* pd_last_error(const pd_ctx* c) { return c ? c->err.c_str() : g_setup_err.c_str(); }
+
+pd_status pd_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, PD_EINVAL, "null output");
+  return pd_comm_unique_id(out128) == 0 ? PD_OK : fail(nullptr, PD_ENCCL, "%s", pd_comm_last_error());
+}
+
+void pd_destroy(pd_ctx* c) {
+  if (c && c->st) cudaStreamSynchronize(c->st);
+  free_ctx(c);
+}
+
+pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme s, const pd_dist* dist,
+                   void* cuda_stream, pd_ctx** out) {
+  if (!out) return fail(nullptr, PD_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!g) return fail(nullptr, PD_EINVAL, "grid is NULL");
+  if (!(alpha > 0.0 && alpha <= 1.0)) return fail(nullptr, PD_EINVAL, "alpha=%g outside (0,1]", alpha);
+  if (!(dt > 0.0)) return fail(nullptr, PD_EINVAL, "dt=%g must be > 0", dt);
+  if (!pd_tfft_supported(nt)) return fail(nullptr, PD_EINVAL, "Nt=%d must be a power of two in [2, 8192]", nt);
+  if (s != PD_BE && s != PD_CN && s != PD_LEAPFROG) return fail(nullptr, PD_EINVAL, "unknown scheme %d", (int)s);
+  if (s == PD_LEAPFROG && nt < 4) return fail(nullptr, PD_EINVAL, "leapfrog needs Nt >= 4");
+  if (!(g->length > 0.0)) return fail(nullptr, PD_EINVAL, "length must be > 0");
+  if (g->op == PD_ADE1D_DIRICHLET || g->op == PD_WAVE1D_DIRICHLET) {
+    if (g->nx < 1 || g->ny != 1) return fail(nullptr, PD_EINVAL, "1D grid needs nx >= 1, ny == 1");
+    if (pd_tridiag_threads(g->nx) < 0) return fail(nullptr, PD_EINVAL, "Nx=%d too large (max %d)", g->nx,
+                                                   1024 * pd_tridiag_rows_per_thread());
+  } else if (g->op == PD_ADE2D_PERIODIC) {
+    if (g->nx != g->ny || !pd_slab2d_supported(g->nx))
+      return fail(nullptr, PD_EINVAL, "2D grid must be N x N with N a power of two in [16, 1024]");
+  } else {
+    return fail(nullptr, PD_EINVAL, "unknown operator %d", (int)g->op);
+  }
+  const int size = dist ? dist->size : 1, rank = dist ? dist->rank : 0;
+  if (size < 1 || rank < 0 || rank >= size) return fail(nullptr, PD_EINVAL, "bad rank/size %d/%d", rank, size);
+
+  pd_ctx* c = new pd_ctx();
+  c->g = *g;
+  c->dt = dt;
+  c->nt = nt;
+  c->F = nt / 2 + 1;
+  c->alpha = alpha;
+  c->scheme = s;
+  c->st = (cudaStream_t)cuda_stream;
+  c->rank = rank;
+  c->size = size;
+  c->Sg = (long long)g->nx * g->ny;
+
+  // ---- distribution: spatial slabs (1D: x-ranges, 2D: y-row ranges) ----
+  {
+    const int ext = g->op == PD_ADE2D_PERIODIC ? g->ny : g->nx;
+    const int base = ext / size, rem = ext % size;
+    const int lo = rank * base + (rank < rem ? rank : rem);
+    const int cnt = base + (rank < rem ? 1 : 0);
+    if (g->op == PD_ADE2D_PERIODIC) {
+      c->nx_loc = g->nx;
+      c->ny_loc = cnt;
+      c->off = (long long)lo * g->nx;
+    } else {
+      c->nx_loc = cnt;
+      c->ny_loc = 1;
+      c->off = lo;
+    }
+    c->S = (long long)c->nx_loc * c->ny_loc;
+  }
+  if (size > 1) {
+    if (!dist->nccl_id) {
+      free_ctx(c);
+      return fail(nullptr, PD_EINVAL, "multi-GPU setup needs an NCCL unique id");
+    }
+    c->comm = pd_comm_create(dist->nccl_id, rank, size, c->st);
+    if (!c->comm) {
+      std::string m = pd_comm_last_error();
+      free_ctx(c);
+      return fail(nullptr, PD_ENCCL, "NCCL init failed: %s", m.c_str());
+    }
+    // the distributed apply (transposes) lives in comm.cpp
+  }
+
+  // ---- spectra, Gamma, twiddles ----
+  std::vector<cld> l1, l2;
+  closed_form_spectra(nt, alpha, dt, s, l1, l2);
+  c->lam1_full.resize(nt);
+  c->lam2_full.resize(nt);
+  for (int n = 0; n < nt; ++n) {
+    c->lam1_full[n] = std::complex<double>((double)l1[n].real(), (double)l1[n].imag());
+    c->lam2_full[n] = std::complex<double>((double)l2[n].real(), (double)l2[n].imag());
+  }
+  std::vector<double> hg(nt), hig(nt);
+  for (int j = 0; j < nt; ++j) {
+    hg[j] = (double)powl((long double)alpha, (long double)j / nt);     // alpha^{j/Nt}  (P:l.163-165)
+    hig[j] = (double)powl((long double)alpha, -(long double)j / nt);   // alpha^{-j/Nt} (P:l.877-880)
+  }
+  auto twiddles = [](int n) {
+    std::vector<double2> t(n);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int j = 0; j < n; ++j) {
+      const long double th = 2.0L * pi * (long double)j / (long double)n;
+      t[j] = make_double2((double)cosl(th), (double)-sinl(th));
+    }
+    return t;
+  };
+  std::vector<double2> htw = twiddles(nt), hl1(c->F), hl2(c->F);
+  for (int n = 0; n < c->F; ++n) {
+    hl1[n] = d2(l1[n]);
+    hl2[n] = d2(l2[n]);
+  }
+  pd_status st = PD_OK;
+#define SETUP_CUDA(expr)                                                                   \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      std::string m_ = cudaGetErrorString(e_);                                             \
+      free_ctx(c);                                                                         \
+      return fail(nullptr, e_ == cudaErrorMemoryAllocation ? PD_ENOMEM : PD_ECUDA, "%s: %s", #expr, m_.c_str()); \
+    }                                                                                      \
+  } while (0)
+  SETUP_CUDA(dalloc(&c->gam, nt));
+  SETUP_CUDA(dalloc(&c->igam, nt));
+  SETUP_CUDA(dalloc(&c->tw_t, nt));
+  SETUP_CUDA(dalloc(&c->lam1, c->F));
+  SETUP_CUDA(dalloc(&c->lam2, c->F));
+  SETUP_CUDA(cudaMemcpy(c->gam, hg.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  SETUP_CUDA(cudaMemcpy(c->igam, hig.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  SETUP_CUDA(cudaMemcpy(c->tw_t, htw.data(), nt * sizeof(double2), cudaMemcpyHostToDevice));
+  SETUP_CUDA(cudaMemcpy(c->lam1, hl1.data(), c->F * sizeof(double2), cudaMemcpyHostToDevice));
+  SETUP_CUDA(cudaMemcpy(c->lam2, hl2.data(), c->F * sizeof(double2), cudaMemcpyHostToDevice));
+
+  // ---- spatial operator ----
+  pd_stencil& sp = c->sten;
+  sp.op = g->op == PD_ADE1D_DIRICHLET ? 0 : g->op == PD_WAVE1D_DIRICHLET ? 1 : 2;
+  sp.scheme = s == PD_BE ? 0 : s == PD_CN ? 1 : 2;
+  sp.nx = c->nx_loc;
+  sp.ny = c->ny_loc;
+  sp.nt = nt;
+  sp.dt = dt;
+  sp.theta = s == PD_BE ? 1.0 : 0.5;
+  if (g->op != PD_ADE2D_PERIODIC) {
+    const double h = g->length / (g->nx + 1);
+    const double nu = g->nu, a = g->op == PD_ADE1D_DIRICHLET ? g->ax : 0.0;
+    sp.sub = -nu / (h * h) - a / (2 * h);
+    sp.dia = 2 * nu / (h * h);
+    sp.sup = -nu / (h * h) + a / (2 * h);
+    std::vector<pd_tri_coef> tc;
+    st = tri_coefs(c, l1, l2, sp.sub, sp.dia, sp.sup, tc);
+    if (st != PD_OK) {
+      std::string m = c->err;
+      free_ctx(c);
+      return fail(nullptr, st, "%s", m.c_str());
+    }
+    SETUP_CUDA(dalloc(&c->tri, c->F));
+    SETUP_CUDA(cudaMemcpy(c->tri, tc.data(), c->F * sizeof(pd_tri_coef), cudaMemcpyHostToDevice));
+  } else {
+    const int N = g->nx;
+    const double h = g->length / N;
+    sp.k2c = 4 * g->nu / (h * h);
+    sp.k2x_m = -g->nu / (h * h) - g->ax / (2 * h);
+    sp.k2x_p = -g->nu / (h * h) + g->ax / (2 * h);
+    sp.k2y_m = -g->nu / (h * h) - g->ay / (2 * h);
+    sp.k2y_p = -g->nu / (h * h) + g->ay / (2 * h);
+    c->slab.kd = 4 * g->nu / (h * h);
+    c->slab.cx = g->ax / h;
+    c->slab.cy = g->ay / h;
+    std::vector<double> hsx(N), hsn(N);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < N; ++k) {
+      const long double sk = sinl(pi * k / N);
+      hsx[k] = (double)(sk * sk);
+      hsn[k] = (double)sinl(2.0L * pi * k / N);
+    }
+    // singularity: min |lambda1 + lambda2 kappa| over the half spectrum and all (kx, ky)
+    long double worst = 1e300L;
+    int wn = -1;
+    for (int n = 0; n < c->F; ++n) {
+      for (int ky = 0; ky < N; ++ky)
+        for (int kx = 0; kx < N; ++kx) {
+          const cld kap((long double)c->slab.kd * (hsx[kx] + hsx[ky]),
+                        (long double)c->slab.cx * hsn[kx] + (long double)c->slab.cy * hsn[ky]);
+          const long double m = std::abs(l1[n] + l2[n] * kap) / (std::abs(l1[n]) + std::abs(l2[n]) * std::abs(kap) + 1e-300L);
+          if (m < worst) {
+            worst = m;
+            wn = n;
+          }
+        }
+    }
+    if (worst < 1e-13L) {
+      free_ctx(c);
+      return fail(nullptr, PD_ESINGULAR, "shifted system singular at frequency n=%d (relative |den| %.3Le)", wn, worst);
+    }
+    std::vector<double2> htws = twiddles(N);
+    SETUP_CUDA(dalloc(&c->sx, N));
+    SETUP_CUDA(dalloc(&c->sn, N));
+    SETUP_CUDA(dalloc(&c->tw_s, N));
+    SETUP_CUDA(cudaMemcpy(c->sx, hsx.data(), N * sizeof(double), cudaMemcpyHostToDevice));
+    SETUP_CUDA(cudaMemcpy(c->sn, hsn.data(), N * sizeof(double), cudaMemcpyHostToDevice));
+    SETUP_CUDA(cudaMemcpy(c->tw_s, htws.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
+    // clusters: cs CTAs per slab, <= ~64 MB of slabs in flight (L2 = 126 MB)
+    int cs = N >= 256 ? 8 : (N >= 64 ? 4 : (N / 8 >= 2 ? 2 : 1));
+    while (cs > 1 && N % (cs * 8) != 0) cs >>= 1;
+    const long long slab_bytes = (long long)N * N * 16;
+    int ncl = (int)std::max(1LL, (64LL << 20) / slab_bytes);
+    int occ = pd_slab2d_max_clusters(N, cs);
+    if (occ > 0 && ncl > occ) ncl = occ;
+    if (ncl > c->F) ncl = c->F;
+    c->slab_cs = cs;
+    c->slab_clusters = ncl;
+  }
+
+  // ---- workspace ----
+  SETUP_CUDA(dalloc(&c->Sh, (size_t)c->F * c->S));
+  SETUP_CUDA(dalloc(&c->rvec, (size_t)nt * c->S));
+  {
+    pd_stencil tmp = sp;
+    const long long Sx = (long long)tmp.nx * tmp.ny;
+    const long long nb = ((Sx + 255) / 256) * ((nt + 31) / 32);
+    c->npartial = (int)std::max<long long>(nb, (long long)pd_blas_blocks() * 32);
+  }
+  SETUP_CUDA(dalloc(&c->partial, (size_t)c->npartial));
+  SETUP_CUDA(dalloc(&c->dred, 64));
+  SETUP_CUDA(cudaMallocHost((void**)&c->hred, 64 * sizeof(double)));
+#undef SETUP_CUDA
+  *out = c;
+  return PD_OK;
+}
+
+pd_status pd_local_shape(const pd_ctx* c, int* nx_local, int* ny_local, long long* offset) {
+  if (!c) return PD_EINVAL;
+  if (nx_local) *nx_local = c->nx_loc;
+  if (ny_local) *ny_local = c->ny_loc;
+  if (offset) *offset = c->off;
+  return PD_OK;
+}
+
+long long pd_local_size(const pd_ctx* c) { return c ? (long long)c->nt * c->S : -1; }
+
+pd_status pd_spectra(const pd_ctx* c, double* l1, double* l2) {
+  if (!c || !l1 || !l2) return PD_EINVAL;
+  for (int n = 0; n < c->nt; ++n) {
+    l1[2 * n] = c->lam1_full[n].real();
+    l1[2 * n + 1] = c->lam1_full[n].imag();
+    l2[2 * n] = c->lam2_full[n].real();
+    l2[2 * n + 1] = c->lam2_full[n].imag();
+  }
+  return PD_OK;
+}
+
+long long pd_kernel_launches(const pd_ctx* c) { return c ? c->launches : -1; }
+
+static void resolve_events(pd_ctx* c) {
+  for (auto& pr : c->evrec) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, c->evpool[pr.second], c->evpool[pr.second + 1]) == cudaSuccess) {
+      c->phase_ms[pr.first] += ms;
+      c->phase_n[pr.first] += 1;
+    }
+  }
+  c->evrec.clear();
+}
+
+pd_status pd_enable_phase_timing(pd_ctx* c, int en) {
+  if (!c) return PD_EINVAL;
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  c->timing = en != 0;
+  c->evrec.clear();
+  for (int i = 0; i < 8; ++i) {
+    c->phase_ms[i] = 0;
+    c->phase_n[i] = 0;
+    c->ev_open[i] = -1;
+  }
+  return PD_OK;
+}
+
+pd_status pd_phase_times(pd_ctx* c, double* ms4, long long* n4) {
+  if (!c) return PD_EINVAL;
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  resolve_events(c);
+  for (int i = 0; i < 8; ++i) {
+    if (ms4) ms4[i] = c->phase_ms[i];
+    if (n4) n4[i] = c->phase_n[i];
+  }
+  return PD_OK;
+}
+
+}  // extern "C"
+
+// ---- phase timing: CUDA events recorded on the context stream around each kernel, resolved lazily
+// (pd_phase_times) so the timed region is not serialised by host syncs ----
+static void phase_begin(pd_ctx* c, int ph) {
+  if (!c->timing) return;
+  const int need = (int)(c->evrec.size() + 1) * 2;
+  while ((int)c->evpool.size() < need) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    c->evpool.push_back(e);
+  }
+  const int i = (int)c->evrec.size() * 2;
+  cudaEventRecord(c->evpool[i], c->st);
+  c->ev_open[ph] = i;
+}
+static void phase_end(pd_ctx* c, int ph) {
+  if (!c->timing || c->ev_open[ph] < 0) return;
+  const int i = c->ev_open[ph];
+  cudaEventRecord(c->evpool[i + 1], c->st);
+  c->evrec.emplace_back(ph, i);
+  c->ev_open[ph] = -1;
+  if (c->evrec.size() >= 2048) {  // bound the pool: resolve (syncs) every 2048 records
+    cudaEventSynchronize(c->evpool[i + 1]);
+    resolve_events(c);
+  }
+}
+
+// Step (b) on the workspace spectrum (local frequencies: all F when size == 1)
+static pd_status spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
+  if (c->g.op == PD_ADE2D_PERIODIC) {
+    PD_LAUNCH(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
+                                  std::min(c->slab_clusters, std::max(1, nfreq)), c->slab_cs, c->st));
+  } else {
+    PD_LAUNCH(c, pd_launch_tridiag(Sh, c->g.nx, nfreq, c->tri + f0, pd_tridiag_rows_per_thread(), c->st));
+  }
+  return PD_OK;
+}
+
+// z = P^{-1} r, or u += P^{-1} r when accumulate
+static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
+  if (c->size > 1) {
+    return pd_comm_apply(c->comm, c, r, z, accumulate) == 0 ? PD_OK
+                                                            : fail(c, PD_ENCCL, "distributed apply: %s", pd_comm_last_error());
+  }
+  phase_begin(c, 0);
+  PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, c->Sh, c->S, c->gam, c->tw_t, c->st));
+  phase_end(c, 0);
+  phase_begin(c, 1);
+  pd_status s = spatial_solve(c, c->Sh, c->F, 0);
+  if (s != PD_OK) return s;
+  phase_end(c, 1);
+  const int ph = accumulate ? 4 : 2;
+  phase_begin(c, ph);
+  PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, c->Sh, z, c->S, c->igam, c->tw_t, accumulate, c->st));
+  phase_end(c, ph);
+  return PD_OK;
+}
+
+// out = b - A u (b != NULL) or A u; if norm2 != NULL: deterministic ||out||^2 into *norm2 (host, syncs)
+static pd_status stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2) {
+  if (c->size > 1) {
+    if (pd_comm_halo_stencil(c->comm, c, b, u, out) != 0)
+      return fail(c, PD_ENCCL, "distributed residual: %s", pd_comm_last_error());
+  } else {
+    int nb = 0;
+    const int ph = b ? 3 : 5;
+    phase_begin(c, ph);
+    PD_LAUNCH(c, pd_launch_stencil(c->sten, b, u, out, c->partial, &nb, c->st));
+    phase_end(c, ph);
+    if (norm2) {
+      PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, nb, 1, c->dred, c->st));
+    }
+  }
+  if (norm2) {
+    if (c->size > 1) {
+      // the distributed stencil leaves the local partial sum in dred[0]
+      if (pd_comm_allreduce_sum(c->comm, c->dred, 1) != 0)
+        return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
+    }
+    PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    PD_CUDA(c, cudaStreamSynchronize(c->st));
+    *norm2 = c->hred[0];
+  }
+  return PD_OK;
+}
+
+// dots[i] = <X[i], y> over the local vector, all-reduced across ranks, copied to host (syncs)
+static pd_status dots_impl(pd_ctx* c, const double* const* X, int k, const double* y, double* host_out) {
+  const long long n = (long long)c->nt * c->S;
+  PD_LAUNCH(c, pd_launch_multidot(X, k, y, n, c->partial, c->st));
+  PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), k, c->dred, c->st));
+  if (c->size > 1 && pd_comm_allreduce_sum(c->comm, c->dred, k) != 0)
+    return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
+  PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  for (int i = 0; i < k; ++i) host_out[i] = c->hred[i];
+  return PD_OK;
+}
+
+extern "C" {
+
+pd_status pd_apply_precond(pd_ctx* c, const double* r, double* z) {
+  if (!c || !r || !z) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  return apply_impl(c, r, z, 0);
+}
+
+pd_status pd_residual(pd_ctx* c, const double* b, const double* u, double* r, double* rnorm2_host) {
+  if (!c || !b || !u || !r) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  return stencil_impl(c, b, u, r, rnorm2_host);
+}
+
+pd_status pd_matvec(pd_ctx* c, const double* u, double* w) {
+  if (!c || !u || !w) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  return stencil_impl(c, nullptr, u, w, nullptr);
+}
+
+pd_status pd_build_rhs(pd_ctx* c, const double* u0, const double* v0, const double* f, double* b) {
+  if (!c || !u0 || !b) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  if (c->size > 1) {
+    if (pd_comm_build_rhs(c->comm, c, u0, v0, f, b) != 0)
+      return fail(c, PD_ENCCL, "distributed rhs: %s", pd_comm_last_error());
+    return PD_OK;
+  }
+  PD_LAUNCH(c, pd_launch_rhs(c->sten, u0, v0, f, b, c->st));
+  return PD_OK;
+}
+
+static void report_push(pd_report* rep, double v) {
+  if (rep && rep->history && rep->history_len < rep->history_cap) rep->history[rep->history_len] = v;
+  if (rep) rep->history_len++;
+}
+
+pd_status pd_solve_stationary(pd_ctx* c, const double* b, double* u, double tol, int maxit, pd_report* rep) {
+  if (!c || !b || !u) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  if (!(tol > 0) || maxit < 0) return fail(c, PD_EINVAL, "tol must be > 0, maxit >= 0");
+  const auto t0 = std::chrono::steady_clock::now();
+  if (rep) rep->history_len = 0;
+  const double* X[1] = {b};
+  double bb = 0;
+  pd_status s = dots_impl(c, X, 1, b, &bb);
+  if (s != PD_OK) return s;
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) {
+    PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * c->nt * c->S, c->st));
+    if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
+    return PD_OK;
+  }
+  int k = 0;
+  double rel = 0;
+  for (;;) {
+    double rr = 0;
+    s = stencil_impl(c, b, u, c->rvec, &rr);  // r = b - A u (eq 5.1)
+    if (s != PD_OK) return s;
+    rel = std::sqrt(rr) / bnorm;
+    if (k > 0) report_push(rep, rel);
+    if (rel <= tol || k >= maxit) break;
+    s = apply_impl(c, c->rvec, u, 1);  // u += P^{-1} r (fused into Step (c))
+    if (s != PD_OK) return s;
+    ++k;
+  }
+  const bool conv = rel <= tol;
+  if (rep) {
+    rep->iterations = k;
+    rep->converged = conv;
+    rep->rel_residual = rel;
+    rep->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return conv ? PD_OK : PD_NOT_CONVERGED;
+}
+
+pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int m, int maxit, pd_report* rep) {
+  if (!c || !b || !u) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  if (!(tol > 0) || maxit < 0 || m < 1 || m > 30) return fail(c, PD_EINVAL, "need tol > 0, maxit >= 0, 1 <= m <= 30");
+  const auto t0 = std::chrono::steady_clock::now();
+  if (rep) rep->history_len = 0;
+  const long long n = (long long)c->nt * c->S;
+  if (c->gm_m < m) {
+    for (double* p : c->V) cudaFree(p);
+    c->V.assign(m + 1, nullptr);
+    for (auto& p : c->V) {
+      cudaError_t e = dalloc(&p, (size_t)n);
+      if (e != cudaSuccess) {
+        for (double*& q : c->V) {
+          if (q) cudaFree(q);
+          q = nullptr;
+        }
+        c->V.clear();
+        c->gm_m = 0;
+        cudaGetLastError();
+        return fail(c, PD_ENOMEM, "GMRES basis (%d vectors of %lld doubles): %s", m + 1, n, cudaGetErrorString(e));
+      }
+    }
+    if (!c->zvec && dalloc(&c->zvec, (size_t)n) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, PD_ENOMEM, "GMRES work vector");
+    }
+    c->gm_m = m;
+  }
+  const double* Xb[1] = {b};
+  double bb = 0;
+  pd_status s = dots_impl(c, Xb, 1, b, &bb);
+  if (s != PD_OK) return s;
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) {
+    PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * n, c->st));
+    if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
+    return PD_OK;
+  }
+  double rr = 0;
+  s = stencil_impl(c, b, u, c->rvec, &rr);
+  if (s != PD_OK) return s;
+  double beta = std::sqrt(rr);
+  int its = 0;
+  bool conv = beta <= tol * bnorm, breakdown = false;
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m);
+  auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
+  while (!conv && its < maxit) {
+    PD_LAUNCH(c, pd_launch_scale(c->V[0], c->rvec, 1.0 / beta, n, c->st));
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int kk = 0;
+    for (int j = 0; j < m; ++j) {
+      s = apply_impl(c, c->V[j], c->zvec, 0);  // z = P^{-1} v_j
+      if (s != PD_OK) return s;
+      ++its;
+      double* w = c->V[j + 1];
+      s = stencil_impl(c, nullptr, c->zvec, w, nullptr);  // w = A z
+      if (s != PD_OK) return s;
+      // CGS2: two passes of classical Gram-Schmidt
+      const double* const* Vp = c->V.data();
+      s = dots_impl(c, Vp, j + 1, w, h.data());
+      if (s != PD_OK) return s;
+      for (int i = 0; i <= j; ++i) y[i] = -h[i];
+      PD_LAUNCH(c, pd_launch_multiaxpy(w, 1.0, Vp, y.data(), j + 1, n, c->st));
+      s = dots_impl(c, Vp, j + 1, w, h2.data());
+      if (s != PD_OK) return s;
+      for (int i = 0; i <= j; ++i) {
+        y[i] = -h2[i];
+        h[i] += h2[i];
+      }
+      PD_LAUNCH(c, pd_launch_multiaxpy(w, 1.0, Vp, y.data(), j + 1, n, c->st));
+      const double* Xw[1] = {w};
+      double ww = 0;
+      s = dots_impl(c, Xw, 1, w, &ww);
+      if (s != PD_OK) return s;
+      const double hn = std::sqrt(ww);
+      for (int i = 0; i <= j; ++i) Hs(i, j) = h[i];
+      Hs(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * Hs(i, j) + sn[i] * Hs(i + 1, j);
+        Hs(i + 1, j) = -sn[i] * Hs(i, j) + cs[i] * Hs(i + 1, j);
+        Hs(i, j) = t;
+      }
+      const double den = std::hypot(Hs(j, j), Hs(j + 1, j));
+      cs[j] = Hs(j, j) / den;
+      sn[j] = Hs(j + 1, j) / den;
+      Hs(j, j) = den;
+      Hs(j + 1, j) = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      kk = j + 1;
+      report_push(rep, std::fabs(gv[j + 1]) / bnorm);
+      if (std::fabs(gv[j + 1]) <= tol * bnorm || its >= maxit) break;
+      if (hn == 0.0) {
+        breakdown = true;
+        break;
+      }
+      PD_LAUNCH(c, pd_launch_scale(w, w, 1.0 / hn, n, c->st));
+    }
+    // y = H^{-1} g, u += P^{-1} (V y)  (final assembly apply, not counted)
+    for (int i = kk - 1; i >= 0; --i) {
+      double t = gv[i];
+      for (int l = i + 1; l < kk; ++l) t -= Hs(i, l) * y[l];
+      y[i] = t / Hs(i, i);
+    }
+    const double* const* Vp = c->V.data();
+    PD_LAUNCH(c, pd_launch_multiaxpy(c->zvec, 0.0, Vp, y.data(), kk, n, c->st));
+    s = apply_impl(c, c->zvec, u, 1);
+    if (s != PD_OK) return s;
+    s = stencil_impl(c, b, u, c->rvec, &rr);
+    if (s != PD_OK) return s;
+    beta = std::sqrt(rr);
+    conv = beta <= tol * bnorm;
+    if (breakdown) break;
+  }
+  if (rep) {
+    rep->iterations = its;
+    rep->converged = conv;
+    rep->rel_residual = beta / bnorm;
+    rep->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  if (conv) return PD_OK;
+  if (breakdown) return fail(c, PD_EBREAKDOWN, "GMRES breakdown at iteration %d, residual %.3e", its, beta / bnorm);
+  return PD_NOT_CONVERGED;
+}
+
+// ---- host-buffer variants ----
+static pd_status ensure_stage(pd_ctx* c) {
+  const size_t n = (size_t)c->nt * c->S;
+  if (!c->stage_a && dalloc(&c->stage_a, n) != cudaSuccess) return fail(c, PD_ENOMEM, "staging buffer");
+  if (!c->stage_b && dalloc(&c->stage_b, n) != cudaSuccess) return fail(c, PD_ENOMEM, "staging buffer");
+  return PD_OK;
+}
+
+pd_status pd_apply_precond_host(pd_ctx* c, const double* rh, double* zh) {
+  if (!c || !rh || !zh) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  pd_status s = ensure_stage(c);
+  if (s != PD_OK) return s;
+  const size_t bytes = sizeof(double) * c->nt * c->S;
+  PD_CUDA(c, cudaMemcpyAsync(c->stage_a, rh, bytes, cudaMemcpyHostToDevice, c->st));
+  s = apply_impl(c, c->stage_a, c->stage_b, 0);
+  if (s != PD_OK) return s;
+  PD_CUDA(c, cudaMemcpyAsync(zh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  return PD_OK;
+}
+
+pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, double tol, int m, int maxit,
+                        pd_report* rep) {
+  if (!c || !bh || !uh) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  pd_status s = ensure_stage(c);
+  if (s != PD_OK) return s;
+  const size_t bytes = sizeof(double) * c->nt * c->S;
+  PD_CUDA(c, cudaMemcpyAsync(c->stage_a, bh, bytes, cudaMemcpyHostToDevice, c->st));
+  PD_CUDA(c, cudaMemcpyAsync(c->stage_b, uh, bytes, cudaMemcpyHostToDevice, c->st));
+  s = solver == 0 ? pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep)
+                  : pd_solve_gmres(c, c->stage_a, c->stage_b, tol, m, maxit, rep);
+  if (s < 0) return s;
+  PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  return s;
+}
+
+}  // extern "C"
+
+// accessors used by comm.cpp (distributed apply)
+pd_ctx_view pd_ctx_get_view(pd_ctx* c) {
+  pd_ctx_view v;
+  v.nt = c->nt;
+  v.F = c->F;
+  v.op = c->g.op;
+  v.nx = c->g.nx;
+  v.ny = c->g.ny;
+  v.nx_loc = c->nx_loc;
+  v.ny_loc = c->ny_loc;
+  v.S = c->S;
+  v.Sg = c->Sg;
+  v.off = c->off;
+  v.st = c->st;
+  v.gam = c->gam;
+  v.igam = c->igam;
+  v.tw_t = c->tw_t;
+  v.sten = c->sten;
+  v.partial = c->partial;
+  v.dred = c->dred;
+  v.Sh = c->Sh;
+  return v;
+}
+int pd_ctx_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) { return spatial_solve(c, Sh, nfreq, f0) == PD_OK ? 0 : -1; }
+void pd_ctx_count_launch(pd_ctx* c, int n) { c->launches += n; }

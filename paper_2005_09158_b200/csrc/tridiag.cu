@@ -1,0 +1,186 @@
+// Step (b), 1D: (lambda_{1,n} I + lambda_{2,n} K) S2_n = S1_n for every frequency n (P:l.182, 816; M = I).
+//
+// K is the constant-coefficient tridiagonal FD operator (Dirichlet), so every shifted system is a Toeplitz
+// tridiagonal  a x_{i-1} + b x_i + c x_{i+1} = d_i  (x_{-1} = x_N = 0) with complex (a, b, c).  With
+// r1, r2 the roots of c r^2 + b r + a = 0 (|r2| <= |r1|), the operator factors exactly as
+//   w_i - r2 w_{i-1} = d_i,   w_i = c (x_{i+1} - r1 x_i),   w_{-1} = c x_0,
+// i.e. a stable forward first-order recurrence (|r2| < 1) followed by a stable backward one
+//   x_i = s x_{i+1} - tau w_i,  s = 1/r1, tau = 1/(c r1)   (|s| < 1),
+// plus one rank-1 correction for the unknown x_0:  x = x^(d) + (c x_0) q, x_0 = x^(d)_0 / (1 - c q_0), where q
+// is the response to w^(1)_i = r2^{i+1}.  tau = 2/(-b -+ sqrt(b^2-4ac)) stays finite when c -> 0 (lower
+// bidiagonal limit) and r2 = a tau, s = c tau.  Setup checks |r2|^N and |s|^N stay bounded (PD_EINVAL).
+// Numerically checked against pivoted banded LU on every frequency of configs 0-2.
+// First-order recurrences with a *uniform* multiplier parallelise as chunked affine scans: a CTA owns one
+// frequency, each thread L consecutive rows in registers, carries cross threads with warp shuffles.
+// HBM traffic: 16 B read + 16 B write per complex unknown (the half spectrum, ~8+8 B per real dof).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int kL = 16;  // rows per thread
+
+PD_D double2 shfl_up2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+PD_D double2 shfl_down2(double2 v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+PD_D double2 cpow_int(double2 m, int e) {
+  double2 r = make_double2(1.0, 0.0);
+  while (e) {
+    if (e & 1) r = cmul(r, m);
+    m = cmul(m, m);
+    e >>= 1;
+  }
+  return r;
+}
+
+// Exclusive affine scan over the CTA's threads: I_k = M I_{k-1} + e_k, returns I_{k-1} (0 for the first).
+// REVERSE scans from the last thread to the first.  tot: smem scratch of NW double2.
+template <int NT, bool REVERSE>
+PD_D double2 block_affine_scan_excl(double2 e, double2 M, double2* tot) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int vl = REVERSE ? 31 - lane : lane;
+  const int vw = REVERSE ? NW - 1 - warp : warp;
+  double2 I = e, Md = M;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    double2 o = REVERSE ? shfl_down2(I, d) : shfl_up2(I, d);
+    if (vl >= d) I = cfma(Md, o, I);
+    Md = cmul(Md, Md);
+  }
+  // Md == M^32 now
+  if (vl == 31) tot[vw] = I;
+  __syncthreads();
+  double2 P = czero();
+  for (int w = 0; w < vw; ++w) P = cfma(Md, P, tot[w]);
+  __syncthreads();
+  I = cfma(cpow_int(M, vl + 1), P, I);  // global inclusive
+  double2 ex = REVERSE ? shfl_down2(I, 1) : shfl_up2(I, 1);
+  return vl == 0 ? P : ex;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) tridiag_kernel(double2* __restrict__ Sh, int N, const pd_tri_coef* __restrict__ coef) {
+  constexpr int L = kL;
+  extern __shared__ double2 sbuf[];           // staging: NT*L + NT (padded rows)
+  __shared__ double2 R2POW[L], SPOW[L + 1], tot[NT / 32], bc[2];
+  const int n = blockIdx.x;
+  const pd_tri_coef cf = coef[n];
+  double2* row = Sh + (long long)n * N;
+
+  if (threadIdx.x == 0) {
+    double2 p = cf.r2, sp = make_double2(1.0, 0.0);
+    for (int j = 0; j < L; ++j) {
+      R2POW[j] = p;  // r2^{j+1}
+      p = cmul(p, cf.r2);
+      SPOW[j] = sp;  // s^j
+      sp = cmul(sp, cf.s);
+    }
+    SPOW[L] = sp;
+  }
+  // coalesced load into padded staging: element i -> i + i/L
+  for (int i = threadIdx.x; i < N; i += NT) sbuf[i + i / L] = __ldcs(row + i);
+  __syncthreads();
+
+  const int k = threadIdx.x;
+  const int i0 = k * L;
+  const int Lk = max(0, min(L, N - i0));
+  double2 d[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) d[j] = (j < Lk) ? sbuf[i0 + j + k] : czero();
+
+  // forward local: w_j = r2 w_{j-1} + d_j (zero carry-in)
+  double2 p = czero();
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    if (j < Lk) {
+      p = cfma(cf.r2, p, d[j]);
+      d[j] = p;
+    }
+  }
+  const double2 Vin = block_affine_scan_excl<NT, false>(p, cf.r2L, tot);
+#pragma unroll
+  for (int j = 0; j < L; ++j)
+    if (j < Lk) d[j] = cfma(R2POW[j], Vin, d[j]);
+
+  // backward local: x_j = s x_{j+1} - tau w_j (zero carry-in from the right)
+  const double2 mtau = cneg(cf.tau);
+  p = czero();
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j) {
+    if (j < Lk) {
+      p = cfma(cf.s, p, cmul(mtau, d[j]));
+      d[j] = p;
+    }
+  }
+  // homogeneous response q (input w_i = r2^{i+1}): chunk-start value with zero carry-in
+  const double2 B = cmul(mtau, cpow_int(cf.r2, i0));  // -tau r2^{i0}
+  double2 pq = czero();
+  for (int j = Lk - 1; j >= 0; --j) pq = cfma(cf.s, pq, cmul(R2POW[j], B));
+  const double2 Xin = block_affine_scan_excl<NT, true>(p, cf.sL, tot);
+  const double2 Qin = block_affine_scan_excl<NT, true>(pq, cf.sL, tot);
+#pragma unroll
+  for (int j = 0; j < L; ++j)
+    if (j < Lk) d[j] = cfma(SPOW[Lk - j], Xin, d[j]);
+  if (k == 0) {
+    const double2 q0 = cfma(SPOW[Lk], Qin, pq);
+    const double2 x0 = cdiv(d[0], csub(make_double2(1.0, 0.0), cmul(cf.c, q0)));  // x^(d)_0 / (1 - c q_0)
+    bc[0] = cmul(cf.c, x0);
+  }
+  __syncthreads();
+  const double2 x0 = bc[0];  // c x_0
+  // x_i += (c x_0) q_i, q_i = q^loc_i + s^{Lk-j} Q_in, q^loc recomputed backward
+  pq = czero();
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j) {
+    if (j < Lk) {
+      pq = cfma(cf.s, pq, cmul(R2POW[j], B));
+      const double2 q = cfma(SPOW[Lk - j], Qin, pq);
+      d[j] = cfma(x0, q, d[j]);
+    }
+  }
+  __syncthreads();  // staging buffer reuse
+#pragma unroll
+  for (int j = 0; j < L; ++j)
+    if (j < Lk) sbuf[i0 + j + k] = d[j];
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += NT) __stcs(row + i, sbuf[i + i / L]);
+}
+
+template <int NT>
+cudaError_t launch_nt(double2* Sh, int nx, int nfreq, const pd_tri_coef* coef, cudaStream_t st) {
+  const int smem = (NT * kL + NT) * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tridiag_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  tridiag_kernel<NT><<<nfreq, NT, smem, st>>>(Sh, nx, coef);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int pd_tridiag_rows_per_thread() { return kL; }
+
+int pd_tridiag_threads(int nx) {
+  int t = 32;
+  while (t * kL < nx) t <<= 1;
+  return t <= 1024 ? t : -1;
+}
+
+cudaError_t pd_launch_tridiag(double2* Sh, int nx, int nfreq, const pd_tri_coef* coef, int, cudaStream_t st) {
+  switch (pd_tridiag_threads(nx)) {
+    case 32: return launch_nt<32>(Sh, nx, nfreq, coef, st);
+    case 64: return launch_nt<64>(Sh, nx, nfreq, coef, st);
+    case 128: return launch_nt<128>(Sh, nx, nfreq, coef, st);
+    case 256: return launch_nt<256>(Sh, nx, nfreq, coef, st);
+    case 512: return launch_nt<512>(Sh, nx, nfreq, coef, st);
+    case 1024: return launch_nt<1024>(Sh, nx, nfreq, coef, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
