@@ -9,6 +9,22 @@ cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S
 cudaError_t pd_launch_tfft_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
                                const double2* tw, int accumulate, cudaStream_t st);
 
+// ---- Steps (a)/(c) for Nt >= 1024: four-step time FFT with an L2-resident scratch (tfft4.cu) ----
+struct pd_tf4_tables {
+  const double2* tw1;  // exp(-2 pi i j / N1), N1 = Nt / 64
+  const double2* tw2;  // exp(-2 pi i j / 64)
+  const double2* twt;  // exp(-2 pi i j / Nt)
+};
+int pd_tf4_supported(int nt);
+int pd_tf4_n2();
+int pd_tf4_pairs_per_tile();
+cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+                              const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
+                              int* nl);
+cudaError_t pd_launch_tf4_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+                              const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, int accumulate,
+                              cudaStream_t st, int* nl);
+
 // ---- Step (b), 1D: batched constant-coefficient complex tridiagonal solves (tridiag.cu) ----
 // Per frequency n (row n of Sh, nx entries): (a_n x_{i-1} + b_n x_i + c_n x_{i+1}) = d_i with
 // a_n = lam2_n*sub, b_n = lam1_n + lam2_n*dia, c_n = lam2_n*sup.  coef[n] holds the host-computed
@@ -33,10 +49,11 @@ struct pd_slab_params {
   double cx, cy; // ax / h, ay / h
 };
 int pd_slab2d_supported(int n);
+int pd_slab2d_chunk(int n, int nfreq);
+// chunk = slabs per L2-resident chunk; *launches = kernels launched
 cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                              const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
-                             int num_clusters, int cluster_size, cudaStream_t st);
-int pd_slab2d_max_clusters(int n, int cluster_size);
+                             int chunk, cudaStream_t st, int* launches);
 
 // ---- all-at-once residual / matvec (stencil.cu) ----
 struct pd_stencil {
@@ -55,16 +72,14 @@ cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double
 cudaError_t pd_launch_rhs(const pd_stencil& p, const double* u0, const double* v0, const double* f, double* b,
                           cudaStream_t st);
 
-// ---- deterministic BLAS-1 (blas1.cu) ----
+// ---- deterministic BLAS-1 for the Krylov loop (blas1.cu) ----
 int pd_blas_blocks();
-// partial[blk*k + i] = sum over block's range of x_i . y  (x_i = X[i], i < k)
-cudaError_t pd_launch_multidot(const double* const* X, int k, const double* y, long long n, double* partial,
-                               cudaStream_t st);
+// mode 0: partial <- <X_i, y>;  1: y <- a y + sum c_i X_i, partial <- <X_i, y_new>;
+// mode 2: y <- a y + sum c_i X_i, partial <- <y_new, y_new>;  3: y <- sum c_i X_i.
+// partial[blk * K' + i], K' = k (modes 0, 1) or 1 (mode 2); coef on the host.  All vectors 16-byte aligned.
+cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coef, int k, double a, double* y,
+                             long long n, double* partial, cudaStream_t st);
 // sum partials in fixed order: out[i] = sum_blk partial[blk*k + i]  (device out)
 cudaError_t pd_launch_reduce_partials(const double* partial, int nblk, int k, double* out, cudaStream_t st);
-// y = alpha*y + sum_i coef[i] * X[i]   (coef on device)
-cudaError_t pd_launch_multiaxpy(double* y, double alpha, const double* const* X, const double* coef, int k,
-                                long long n, cudaStream_t st);
-// y = a*x (+ y if accumulate)
-cudaError_t pd_launch_scale(double* y, const double* x, double a, long long n, cudaStream_t st);
-cudaError_t pd_launch_axpy(double* y, const double* x, double a, long long n, cudaStream_t st);
+// y = a x + b y
+cudaError_t pd_launch_axpby(double* y, const double* x, double a, double b, long long n, cudaStream_t st);

@@ -11,6 +11,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -39,6 +40,11 @@ struct pd_ctx {
   double* gam = nullptr;
   double* igam = nullptr;
   double2* tw_t = nullptr;       // exp(-2 pi i j / Nt)
+  double2* tw_n1 = nullptr;      // four-step tables (Nt >= 1024)
+  double2* tw_n2 = nullptr;
+  double2* tf4_scratch = nullptr;
+  long long tf4_chunk = 0;
+  bool use_tf4 = false;
   double2* lam1 = nullptr;       // half spectrum, F entries
   double2* lam2 = nullptr;
   pd_tri_coef* tri = nullptr;    // 1D
@@ -46,7 +52,7 @@ struct pd_ctx {
   double* sn = nullptr;          // 2D: sin(2 pi k / N)
   double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
   pd_slab_params slab{};
-  int slab_clusters = 0, slab_cs = 0;
+  int slab_chunk = 1;
   pd_stencil sten{};
   // host copies
   std::vector<std::complex<double>> lam1_full, lam2_full;
@@ -191,7 +197,7 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
 
 static void free_ctx(pd_ctx* c) {
   if (!c) return;
-  void* ptrs[] = {c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
+  void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -401,16 +407,31 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     SETUP_CUDA(cudaMemcpy(c->sx, hsx.data(), N * sizeof(double), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->sn, hsn.data(), N * sizeof(double), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->tw_s, htws.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
-    // clusters: cs CTAs per slab, <= ~64 MB of slabs in flight (L2 = 126 MB)
-    int cs = N >= 256 ? 8 : (N >= 64 ? 4 : (N / 8 >= 2 ? 2 : 1));
-    while (cs > 1 && N % (cs * 8) != 0) cs >>= 1;
-    const long long slab_bytes = (long long)N * N * 16;
-    int ncl = (int)std::max(1LL, (64LL << 20) / slab_bytes);
-    int occ = pd_slab2d_max_clusters(N, cs);
-    if (occ > 0 && ncl > occ) ncl = occ;
-    if (ncl > c->F) ncl = c->F;
-    c->slab_cs = cs;
-    c->slab_clusters = ncl;
+    c->slab_chunk = pd_slab2d_chunk(N, c->F);
+    if (const char* e = getenv("PD_SLAB_CHUNK_MB")) {
+      const long long sb = (long long)N * N * 16;
+      c->slab_chunk = (int)std::max(1LL, std::min<long long>(c->F, (atoll(e) << 20) / sb));
+    }
+  }
+
+  // ---- four-step time FFT for long time axes ----
+  c->use_tf4 = pd_tf4_supported(nt) && getenv("PD_NO_TF4") == nullptr;
+  if (c->use_tf4) {
+    const int n2 = pd_tf4_n2(), n1 = nt / n2, ppt = pd_tf4_pairs_per_tile();
+    std::vector<double2> h1 = twiddles(n1), h2 = twiddles(n2);
+    SETUP_CUDA(dalloc(&c->tw_n1, n1));
+    SETUP_CUDA(dalloc(&c->tw_n2, n2));
+    SETUP_CUDA(cudaMemcpy(c->tw_n1, h1.data(), n1 * sizeof(double2), cudaMemcpyHostToDevice));
+    SETUP_CUDA(cudaMemcpy(c->tw_n2, h2.data(), n2 * sizeof(double2), cudaMemcpyHostToDevice));
+    const long long npairs = (c->S + 1) / 2;
+    // column chunk of the stage-1 -> stage-2 scratch (default 1 GB: launch count beats L2 residency, §5)
+    const char* mb_env = getenv("PD_TF4_CHUNK_MB");
+    const long long mb = mb_env ? atoll(mb_env) : 1024;
+    long long chunk = ((mb << 20) / ((long long)nt * 16)) / ppt * ppt;
+    if (chunk < ppt) chunk = ppt;
+    if (chunk > npairs) chunk = (npairs + ppt - 1) / ppt * ppt;
+    c->tf4_chunk = chunk;
+    SETUP_CUDA(dalloc(&c->tf4_scratch, (size_t)nt * chunk));
   }
 
   // ---- workspace ----
@@ -419,7 +440,7 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   {
     pd_stencil tmp = sp;
     const long long Sx = (long long)tmp.nx * tmp.ny;
-    const long long nb = ((Sx + 255) / 256) * ((nt + 31) / 32);
+    const long long nb = ((Sx + 255) / 256) * ((nt + 63) / 64);
     c->npartial = (int)std::max<long long>(nb, (long long)pd_blas_blocks() * 32);
   }
   SETUP_CUDA(dalloc(&c->partial, (size_t)c->npartial));
@@ -519,8 +540,10 @@ static void phase_end(pd_ctx* c, int ph) {
 // Step (b) on the workspace spectrum (local frequencies: all F when size == 1)
 static pd_status spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   if (c->g.op == PD_ADE2D_PERIODIC) {
-    PD_LAUNCH(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
-                                  std::min(c->slab_clusters, std::max(1, nfreq)), c->slab_cs, c->st));
+    int nl = 0;
+    PD_CUDA(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
+                                c->slab_chunk, c->st, &nl));
+    c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tridiag(Sh, c->g.nx, nfreq, c->tri + f0, pd_tridiag_rows_per_thread(), c->st));
   }
@@ -533,8 +556,15 @@ static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulat
     return pd_comm_apply(c->comm, c, r, z, accumulate) == 0 ? PD_OK
                                                             : fail(c, PD_ENCCL, "distributed apply: %s", pd_comm_last_error());
   }
+  const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   phase_begin(c, 0);
-  PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, c->Sh, c->S, c->gam, c->tw_t, c->st));
+  if (c->use_tf4) {
+    int nl = 0;
+    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, c->Sh, c->S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
+    c->launches += nl;
+  } else {
+    PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, c->Sh, c->S, c->gam, c->tw_t, c->st));
+  }
   phase_end(c, 0);
   phase_begin(c, 1);
   pd_status s = spatial_solve(c, c->Sh, c->F, 0);
@@ -542,7 +572,14 @@ static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulat
   phase_end(c, 1);
   const int ph = accumulate ? 4 : 2;
   phase_begin(c, ph);
-  PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, c->Sh, z, c->S, c->igam, c->tw_t, accumulate, c->st));
+  if (c->use_tf4) {
+    int nl = 0;
+    PD_CUDA(c, pd_launch_tf4_inv(c->nt, c->Sh, z, c->S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate,
+                                 c->st, &nl));
+    c->launches += nl;
+  } else {
+    PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, c->Sh, z, c->S, c->igam, c->tw_t, accumulate, c->st));
+  }
   phase_end(c, ph);
   return PD_OK;
 }
@@ -575,17 +612,31 @@ static pd_status stencil_impl(pd_ctx* c, const double* b, const double* u, doubl
   return PD_OK;
 }
 
-// dots[i] = <X[i], y> over the local vector, all-reduced across ranks, copied to host (syncs)
-static pd_status dots_impl(pd_ctx* c, const double* const* X, int k, const double* y, double* host_out) {
+// Krylov sweep (blas1.cu) over the local vector; the k (or 1) reduced values all-reduced across ranks and
+// copied to host_out (syncs) unless host_out == NULL (mode 3)
+static pd_status krylov_impl(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a,
+                             double* y, double* host_out) {
   const long long n = (long long)c->nt * c->S;
-  PD_LAUNCH(c, pd_launch_multidot(X, k, y, n, c->partial, c->st));
-  PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), k, c->dred, c->st));
-  if (c->size > 1 && pd_comm_allreduce_sum(c->comm, c->dred, k) != 0)
-    return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
-  PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  PD_CUDA(c, cudaStreamSynchronize(c->st));
-  for (int i = 0; i < k; ++i) host_out[i] = c->hred[i];
+  phase_begin(c, 6);
+  PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st));
+  if (mode != 3) {
+    const int kk = mode == 2 ? 1 : k;
+    PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), kk, c->dred, c->st));
+    phase_end(c, 6);
+    if (c->size > 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
+      return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
+    PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, kk * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    PD_CUDA(c, cudaStreamSynchronize(c->st));
+    for (int i = 0; i < kk; ++i) host_out[i] = c->hred[i];
+  } else {
+    phase_end(c, 6);
+  }
   return PD_OK;
+}
+
+// dots[i] = <X[i], y>
+static pd_status dots_impl(pd_ctx* c, const double* const* X, int k, const double* y, double* host_out) {
+  return krylov_impl(c, 0, X, nullptr, k, 0.0, const_cast<double*>(y), host_out);
 }
 
 extern "C" {
@@ -697,44 +748,47 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
     return PD_OK;
   }
+  // Basis kept scaled: V_i = sc[i] * X_i with X_i = c->V[i] in memory, so normalising costs no sweep.
   double rr = 0;
-  s = stencil_impl(c, b, u, c->rvec, &rr);
+  s = stencil_impl(c, b, u, c->V[0], &rr);  // X_0 = r = b - A u
   if (s != PD_OK) return s;
   double beta = std::sqrt(rr);
   int its = 0;
   bool conv = beta <= tol * bnorm, breakdown = false;
-  std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m);
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m), coef(m + 1), sc(m + 1);
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
+  const double* const* Xp = c->V.data();
   while (!conv && its < maxit) {
-    PD_LAUNCH(c, pd_launch_scale(c->V[0], c->rvec, 1.0 / beta, n, c->st));
+    sc[0] = 1.0 / beta;
     std::fill(gv.begin(), gv.end(), 0.0);
     gv[0] = beta;
     int kk = 0;
     for (int j = 0; j < m; ++j) {
-      s = apply_impl(c, c->V[j], c->zvec, 0);  // z = P^{-1} v_j
+      // w_raw = A P^{-1} X_j;  true w = sc[j] * w_raw
+      s = apply_impl(c, c->V[j], c->zvec, 0);
       if (s != PD_OK) return s;
       ++its;
       double* w = c->V[j + 1];
-      s = stencil_impl(c, nullptr, c->zvec, w, nullptr);  // w = A z
+      s = stencil_impl(c, nullptr, c->zvec, w, nullptr);
       if (s != PD_OK) return s;
-      // CGS2: two passes of classical Gram-Schmidt
-      const double* const* Vp = c->V.data();
-      s = dots_impl(c, Vp, j + 1, w, h.data());
-      if (s != PD_OK) return s;
-      for (int i = 0; i <= j; ++i) y[i] = -h[i];
-      PD_LAUNCH(c, pd_launch_multiaxpy(w, 1.0, Vp, y.data(), j + 1, n, c->st));
-      s = dots_impl(c, Vp, j + 1, w, h2.data());
+      // CGS2: h_i = <V_i, w> = sc_i sc_j <X_i, w_raw>;  w_raw -= sum (h_i sc_i / sc_j) X_i  (fused with 2nd dots)
+      s = krylov_impl(c, 0, Xp, nullptr, j + 1, 0.0, w, h.data());
       if (s != PD_OK) return s;
       for (int i = 0; i <= j; ++i) {
-        y[i] = -h2[i];
+        h[i] *= sc[i] * sc[j];
+        coef[i] = -h[i] * sc[i] / sc[j];
+      }
+      s = krylov_impl(c, 1, Xp, coef.data(), j + 1, 1.0, w, h2.data());
+      if (s != PD_OK) return s;
+      for (int i = 0; i <= j; ++i) {
+        h2[i] *= sc[i] * sc[j];
+        coef[i] = -h2[i] * sc[i] / sc[j];
         h[i] += h2[i];
       }
-      PD_LAUNCH(c, pd_launch_multiaxpy(w, 1.0, Vp, y.data(), j + 1, n, c->st));
-      const double* Xw[1] = {w};
       double ww = 0;
-      s = dots_impl(c, Xw, 1, w, &ww);
+      s = krylov_impl(c, 2, Xp, coef.data(), j + 1, 1.0, w, &ww);
       if (s != PD_OK) return s;
-      const double hn = std::sqrt(ww);
+      const double hn = sc[j] * std::sqrt(ww);
       for (int i = 0; i <= j; ++i) Hs(i, j) = h[i];
       Hs(j + 1, j) = hn;
       for (int i = 0; i < j; ++i) {
@@ -756,7 +810,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
         breakdown = true;
         break;
       }
-      PD_LAUNCH(c, pd_launch_scale(w, w, 1.0 / hn, n, c->st));
+      sc[j + 1] = sc[j] / hn;  // V_{j+1} = w / hn = (sc_j / hn) X_{j+1}
     }
     // y = H^{-1} g, u += P^{-1} (V y)  (final assembly apply, not counted)
     for (int i = kk - 1; i >= 0; --i) {
@@ -764,11 +818,12 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
       for (int l = i + 1; l < kk; ++l) t -= Hs(i, l) * y[l];
       y[i] = t / Hs(i, i);
     }
-    const double* const* Vp = c->V.data();
-    PD_LAUNCH(c, pd_launch_multiaxpy(c->zvec, 0.0, Vp, y.data(), kk, n, c->st));
+    for (int i = 0; i < kk; ++i) coef[i] = y[i] * sc[i];
+    s = krylov_impl(c, 3, Xp, coef.data(), kk, 0.0, c->zvec, nullptr);
+    if (s != PD_OK) return s;
     s = apply_impl(c, c->zvec, u, 1);
     if (s != PD_OK) return s;
-    s = stencil_impl(c, b, u, c->rvec, &rr);
+    s = stencil_impl(c, b, u, c->V[0], &rr);  // true residual, also the restart vector X_0
     if (s != PD_OK) return s;
     beta = std::sqrt(rr);
     conv = beta <= tol * bnorm;

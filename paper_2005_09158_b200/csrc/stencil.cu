@@ -9,7 +9,7 @@
 
 namespace {
 
-constexpr int kTC = 32;     // time rows per thread
+constexpr int kTC = 64;     // time rows per thread
 constexpr int kBX = 256;    // threads per block
 
 struct Taps {
@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kBX) stencil1d_kernel(pd_stencil p, const doub
     if (n0 - 2 >= 0) h2 = load1(u + (long long)(n0 - 2) * nx, x, nx);
   }
   const int n1 = min(n0 + kTC, p.nt);
+#pragma unroll 8
   for (int n = n0; n < n1; ++n) {
     N1 h0 = {0, 0, 0};
     if (act) h0 = load1(u + (long long)n * nx, x, nx);
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(kBX) stencil2d_kernel(pd_stencil p, const doub
     if (n0 - 2 >= 0) h2 = load2(u + (n0 - 2) * S, x, y, nx, ny);
   }
   const int n1 = min(n0 + kTC, p.nt);
+#pragma unroll 4
   for (int n = n0; n < n1; ++n) {
     N2 h0 = {0, 0, 0, 0, 0};
     if (act) h0 = load2(u + n * S, x, y, nx, ny);

@@ -17,68 +17,73 @@ namespace {
 
 template <int N>
 struct TileCfg {
-  static constexpr int C = (8192 / N) < 32 ? (8192 / N) : 32;  // complex sequences per tile
+  static constexpr int TILE = N >= 4096 ? 8192 : 4096;                     // complex elements per tile
+  static constexpr int C = (TILE / N) < 32 ? (TILE / N) : 32;             // complex sequences per tile
   static constexpr int E = elems_per_thread(N);
   static constexpr int NTH = C * N / E;
-  static constexpr int R0 = radix_of(N, 0);
-  static constexpr int P = num_passes(N);
+  static constexpr int MINB = NTH <= 256 ? 2 : 1;
 };
 
 // ---------------------------------------------------------------------------------------------
 // Step (a): r (real) -> Gamma r -> FFT over time -> half spectrum.
 // ---------------------------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(TileCfg<N>::NTH)
+__global__ void __launch_bounds__(TileCfg<N>::NTH, TileCfg<N>::MINB)
 tfft_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long long S,
                 const double* __restrict__ gam, const double2* __restrict__ tw) {
   using T = TileCfg<N>;
-  constexpr int C = T::C, NTH = T::NTH, R0 = T::R0;
+  constexpr int C = T::C, NTH = T::NTH;
+  constexpr bool SMT = N <= 1024;  // stage twiddles and Gamma in shared memory
   extern __shared__ double2 sm[];
+  __shared__ double2 s_tw[SMT ? N : 1];
+  __shared__ double s_g[SMT ? N : 1];
   const long long s0 = (long long)blockIdx.x * (2 * C);
-
-  // pass 0 straight from HBM (LS = 1: no inter-pass twiddles), Gamma fused into the load
-  {
-    constexpr int BPT = (C * N / R0) / NTH;
-    double2 v[BPT][R0];
-#pragma unroll
-    for (int bi = 0; bi < BPT; ++bi) {
-      const int b = threadIdx.x + bi * NTH;
-      const int c = b % C, j = b / C;
-      const long long col = s0 + 2 * c;
-#pragma unroll
-      for (int m = 0; m < R0; ++m) {
-        const int t = j + m * (N / R0);
-        const double g = __ldg(gam + t);
-        const double* row = r + (long long)t * S;
-        const double x = col < S ? __ldcs(row + col) : 0.0;
-        const double y = col + 1 < S ? __ldcs(row + col + 1) : 0.0;
-        v[bi][m] = make_double2(g * x, g * y);
-      }
-    }
-#pragma unroll
-    for (int bi = 0; bi < BPT; ++bi) {
-      const int b = threadIdx.x + bi * NTH;
-      const int c = b % C, j = b / C;
-      DFT<R0, false>::run(v[bi]);
-#pragma unroll
-      for (int q = 0; q < R0; ++q) sm[sidx<N, C, false>(j * R0 + q, c)] = v[bi][q];
-    }
+  const double* rc = r + s0;
+  const bool full = s0 + 2 * C <= S;
+  if (SMT) {
+    load_table(s_tw, tw, N);
+    for (int i = threadIdx.x; i < N; i += NTH) s_g[i] = __ldg(gam + i);
     __syncthreads();
   }
-  Passes<N, C, 1, T::P, false, false, NTH>::run(sm, tw);
-
+  // pass 0 straight from HBM with Gamma fused: sequence c = columns (s0+2c) + i (s0+2c+1)
+  constexpr int R0 = first_radix(N), RL = last_radix(N);
+  fft_io<N, C, false, false, NTH, false, true>(
+      sm, SMT ? s_tw : tw,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value;
+        const double* q = rc + (long long)j * S + 2 * c;
+        const long long step = (long long)s * S;
+        const bool okx = full || s0 + 2 * c < S, oky = full || s0 + 2 * c + 1 < S;
+#pragma unroll
+        for (int m = 0; m < R0; ++m) {
+          const int t = j + m * s;
+          const double g = SMT ? s_g[t] : __ldg(gam + t);
+          const double x = okx ? __ldcs(q + m * step) : 0.0;
+          const double y = oky ? __ldcs(q + m * step + 1) : 0.0;
+          v[m] = make_double2(g * x, g * y);
+        }
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value;
+        const int a = lin<N, C, false>(j, c);
+#pragma unroll
+        for (int m = 0; m < RL; ++m) sm[soff<s * C>(a, m)] = w[m];
+      });
+  __syncthreads();
   // separate the two real columns: X_n = (Z_n + conj Z_{N-n})/2, Y_n = -i (Z_n - conj Z_{N-n})/2
   constexpr int NOUT = (N / 2 + 1) * 2 * C;
+  double2* out = Sh + s0;
+#pragma unroll 4
   for (int o = threadIdx.x; o < NOUT; o += NTH) {
     const int col = o % (2 * C), n = o / (2 * C), c = col >> 1;
     const double2 z1 = sm[sidx<N, C, false>(n, c)];
     const double2 z2 = sm[sidx<N, C, false>((N - n) & (N - 1), c)];
-    double2 out;
+    double2 v;
     if (col & 1)
-      out = make_double2(0.5 * (z1.y + z2.y), -0.5 * (z1.x - z2.x));
+      v = make_double2(0.5 * (z1.y + z2.y), -0.5 * (z1.x - z2.x));
     else
-      out = make_double2(0.5 * (z1.x + z2.x), 0.5 * (z1.y - z2.y));
-    if (s0 + col < S) Sh[(long long)n * S + s0 + col] = out;
+      v = make_double2(0.5 * (z1.x + z2.x), 0.5 * (z1.y - z2.y));
+    if (full || s0 + col < S) __stcs(out + (long long)n * S + col, v);
   }
 }
 
@@ -87,102 +92,71 @@ tfft_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long lon
 // MODE 0: z = result.  MODE 1: z += result (fused stationary update u <- u + P^{-1} r).
 // ---------------------------------------------------------------------------------------------
 template <int N, int MODE>
-__global__ void __launch_bounds__(TileCfg<N>::NTH)
+__global__ void __launch_bounds__(TileCfg<N>::NTH, TileCfg<N>::MINB)
 tfft_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long long S,
                 const double* __restrict__ igam, const double2* __restrict__ tw) {
   using T = TileCfg<N>;
-  constexpr int C = T::C, NTH = T::NTH, R0 = T::R0, P = T::P;
+  constexpr int C = T::C, NTH = T::NTH;
+  constexpr bool SMT = N <= 1024;
   extern __shared__ double2 sm[];
+  __shared__ double2 s_tw[SMT ? N : 1];
+  __shared__ double s_g[SMT ? N : 1];
   const long long s0 = (long long)blockIdx.x * (2 * C);
-
-  // load the half-spectrum tile H[n][col], n = 0..N/2, col = 0..2C-1
+  const bool full = s0 + 2 * C <= S;
+  if (SMT) {
+    load_table(s_tw, tw, N);
+    for (int i = threadIdx.x; i < N; i += NTH) s_g[i] = __ldg(igam + i) * (1.0 / N);
+  }
+  if (MODE) {  // warm L2 with the rows of z this tile will read-modify-write
+    for (int t = threadIdx.x; t < N; t += NTH) asm volatile("prefetch.global.L2 [%0];" ::"l"(z + (long long)t * S + s0));
+  }
+  // stage the half-spectrum tile H[n][col], n = 0..N/2, col = 0..2C-1 (coalesced rows)
   constexpr int NIN = (N / 2 + 1) * 2 * C;
+  const double2* in = Sh + s0;
+#pragma unroll 4
   for (int o = threadIdx.x; o < NIN; o += NTH) {
     const int col = o % (2 * C), n = o / (2 * C);
-    sm[pad(o)] = (s0 + col < S) ? __ldcs(Sh + (long long)n * S + s0 + col) : czero();
-  }
-  __syncthreads();
-
-  constexpr int BPT = (C * N / R0) / NTH;
-  double2 v[BPT][R0];
-  // pass 0 input: Z[pos] = X[pos] + i Y[pos], with X[N-n] = conj X[n] for n > N/2
-#pragma unroll
-  for (int bi = 0; bi < BPT; ++bi) {
-    const int b = threadIdx.x + bi * NTH;
-    const int c = b % C, j = b / C;
-#pragma unroll
-    for (int m = 0; m < R0; ++m) {
-      const int pos = j + m * (N / R0);
-      double2 X, Y;
-      if (pos <= N / 2) {
-        X = sm[pad(pos * 2 * C + 2 * c)];
-        Y = sm[pad(pos * 2 * C + 2 * c + 1)];
-      } else {
-        X = cconj(sm[pad((N - pos) * 2 * C + 2 * c)]);
-        Y = cconj(sm[pad((N - pos) * 2 * C + 2 * c + 1)]);
-      }
-      v[bi][m] = make_double2(X.x - Y.y, X.y + Y.x);
-    }
+    sm[pad(o)] = (full || s0 + col < S) ? __ldcs(in + (long long)n * S + col) : czero();
   }
   __syncthreads();
   const double invN = 1.0 / N;
-  if constexpr (P == 1) {
-    // single pass: output natural order, write HBM directly
+  double* zc = z + s0;
+  constexpr int R0 = first_radix(N), RL = last_radix(N);
+  fft_io<N, C, true, false, NTH, true, false>(
+      sm, SMT ? s_tw : tw,
+      [&](int j, auto st, int c, double2* v) {  // Z[pos] = X[pos] + i Y[pos], X[N-n] = conj X[n]
+        constexpr int s = decltype(st)::value;
 #pragma unroll
-    for (int bi = 0; bi < BPT; ++bi) {
-      const int b = threadIdx.x + bi * NTH;
-      const int c = b % C;
-      DFT<R0, true>::run(v[bi]);
-      const long long col = s0 + 2 * c;
+        for (int m = 0; m < R0; ++m) {
+          const int pos = j + m * s;
+          const bool lo = pos <= N / 2;
+          const int pp = lo ? pos : N - pos;
+          const double sg = lo ? 1.0 : -1.0;
+          const double2 X = sm[pad(pp * 2 * C + 2 * c)];
+          const double2 Y = sm[pad(pp * 2 * C + 2 * c + 1)];
+          // conj when pos > N/2: X = (X.x, sg X.y), Y = (Y.x, sg Y.y);  Z = X + i Y
+          v[m] = make_double2(fma(-sg, Y.y, X.x), fma(sg, X.y, Y.x));
+        }
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value;
+        double* q = zc + (long long)j * S + 2 * c;
+        const long long step = (long long)s * S;
+        const bool okx = full || s0 + 2 * c < S, oky = full || s0 + 2 * c + 1 < S;
 #pragma unroll
-      for (int q = 0; q < R0; ++q) {
-        const double g = __ldg(igam + q) * invN;
-        double* row = z + (long long)q * S;
-        if (col < S) row[col] = MODE ? row[col] + g * v[bi][q].x : g * v[bi][q].x;
-        if (col + 1 < S) row[col + 1] = MODE ? row[col + 1] + g * v[bi][q].y : g * v[bi][q].y;
-      }
-    }
-    return;
-  } else {
-#pragma unroll
-    for (int bi = 0; bi < BPT; ++bi) {
-      const int b = threadIdx.x + bi * NTH;
-      const int c = b % C, j = b / C;
-      DFT<R0, true>::run(v[bi]);
-#pragma unroll
-      for (int q = 0; q < R0; ++q) sm[sidx<N, C, false>(j * R0 + q, c)] = v[bi][q];
-    }
-    __syncthreads();
-    Passes<N, C, 1, P - 1, true, false, NTH>::run(sm, tw);
-
-    // last pass: smem -> registers -> HBM (output position j + q*LS, LS = N/R)
-    constexpr int RL = radix_of(N, P - 1), LS = ls_of(N, P - 1);
-    constexpr int BL = (C * N / RL) / NTH;
-    double2 w[BL][RL];
-#pragma unroll
-    for (int bi = 0; bi < BL; ++bi) {
-      const int b = threadIdx.x + bi * NTH;
-      const int c = b % C, j = b / C;
-#pragma unroll
-      for (int m = 0; m < RL; ++m) w[bi][m] = sm[sidx<N, C, false>(j + m * (N / RL), c)];
-    }
-#pragma unroll
-    for (int bi = 0; bi < BL; ++bi) {
-      const int b = threadIdx.x + bi * NTH;
-      const int c = b % C, j = b / C;
-      pass_twiddles<N, RL, LS, true>(w[bi], j, tw);
-      DFT<RL, true>::run(w[bi]);
-      const long long col = s0 + 2 * c;
-#pragma unroll
-      for (int q = 0; q < RL; ++q) {
-        const int t = j + q * LS;
-        const double g = __ldg(igam + t) * invN;
-        double* row = z + (long long)t * S;
-        if (col < S) row[col] = MODE ? row[col] + g * w[bi][q].x : g * w[bi][q].x;
-        if (col + 1 < S) row[col + 1] = MODE ? row[col + 1] + g * w[bi][q].y : g * w[bi][q].y;
-      }
-    }
-  }
+        for (int m = 0; m < RL; ++m) {
+          const int t = j + m * s;
+          const double g = SMT ? s_g[t] : __ldg(igam + t) * invN;
+          double* row = q + m * step;
+          if (MODE) {
+            if (okx) row[0] = fma(g, w[m].x, row[0]);
+            if (oky) row[1] = fma(g, w[m].y, row[1]);
+          } else {
+            if (okx) __stcs(row, g * w[m].x);
+            if (oky) __stcs(row + 1, g * w[m].y);
+          }
+        }
+      });
 }
 
 template <int N>

@@ -1,0 +1,403 @@
+// Steps (a)/(c) for long time axes (Nt >= 1024): four-step time FFT, Nt = N1 * N2 (N2 = 64).
+//
+//   forward:  X[n2 + N2 n1] = sum_t1 w_N1^{t1 n1} [ w_Nt^{t1 n2} sum_t2 x[t1 + N1 t2] w_N2^{t2 n2} ]
+//   inverse:  x[t1 + N1 t2] = sum_n2 w_N2^{-t2 n2} [ w_Nt^{-t1 n2} sum_n1 X[n2 + N2 n1] w_N1^{-t1 n1} ]
+// (same maps as tfft.cu: Step (a) S1 = F Gamma r, Step (c) z = Gamma^{-1} F^* S2 / Nt, eq 2.12, P:l.813-817;
+//  Matlab fft/ifft pairing P:l.864-875).  Two real spatial columns are packed into one complex sequence
+// ("pair" p = columns 2p, 2p+1) and separated again on the half spectrum (reading c15).
+//
+// Why: a single-tile time FFT of Nt = 2048-4096 complex points needs 64-128 KB of shared memory per
+// handful of columns, which leaves one CTA per SM (no load/compute overlap) and 32-64 B HBM row
+// segments.  Here every stage touches 64 rows x 32 pairs (512 B segments, 32 KB tiles, several CTAs
+// per SM); the intermediate Y (complex, Nt x pairs) lives in a scratch buffer processed in column chunks.
+// Measured on B200 (cfg4): per-chunk launches of L2-resident chunks (<= 64 MB) are launch/ramp bound
+// (~18 us per launch), while chunks of ~1 GB run the two stages at ~6.3 TB/s of actual DRAM traffic with
+// the intermediate going through HBM (16 B/dof extra); the default is the latter.  A
+// persistent task-queue variant and a cp.async.bulk-pipelined variant were both measured slower.
+#include <cstdlib>
+
+#include "fft.cuh"
+#include "kernels.h"
+
+using namespace pdfft;
+
+namespace {
+
+constexpr int kP = 32;   // pairs (complex sequences) per tile in stage 1
+constexpr int kN2 = 64;  // stage-1 FFT length
+
+template <int N>
+struct Cfg2 {  // stage FFT of length N over C sequences
+  static constexpr int E = elems_per_thread(N);
+};
+
+// ---------------------------------------------------------------------------------------------
+// forward stage 1: for fixed t1 (blockIdx.y): N2-point FFT over t2 of rows t1 + N1 t2 of P pairs,
+// times w_Nt^{t1 n2}; writes Y[t1][n2][pl] (scratch rows of Pc pairs).
+// ---------------------------------------------------------------------------------------------
+template <int NT, bool VEC, int RM = 16>
+__global__ void __launch_bounds__(kP * kN2 / RM) tf4_fwd_s1(const double* __restrict__ r, long long S, long long p_begin,
+                                                           long long npairs_chunk, double2* __restrict__ Y,
+                                                           const double* __restrict__ gam,
+                                                           const double2* __restrict__ tw2,
+                                                           const double2* __restrict__ twt) {
+  constexpr int N1 = NT / kN2, C = kP, NTH = kP * kN2 / RM;
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw2[kN2], s_twr[kN2];  // 64-point twiddles; w_Nt^{t1 n2}, n2 < 64
+  __shared__ double s_g[kN2];                 // Gamma of rows t1 + N1 t2
+  const int t1 = blockIdx.y;
+  const long long pl0 = (long long)blockIdx.x * kP;  // pair index within the chunk
+  const long long p0 = p_begin + pl0;                // global pair index
+  const long long Pc = npairs_chunk;
+  for (int i = threadIdx.x; i < kN2; i += NTH) {
+    s_tw2[i] = __ldg(tw2 + i);
+    s_twr[i] = __ldg(twt + t1 * i);
+    s_g[i] = __ldg(gam + t1 + N1 * i);
+  }
+  __syncthreads();
+  const bool fullp = pl0 + kP <= Pc;
+  fft_io<kN2, C, false, false, NTH, false, false, RM>(
+      sm, s_tw2,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(kN2, RM);
+        const long long col = 2 * (p0 + c);
+        const double* q = r + (long long)(t1 + N1 * j) * S + col;
+        const long long step = (long long)N1 * s * S;
+        const bool ok = fullp || pl0 + c < Pc;
+        const bool okx = ok && (VEC || col < S), oky = ok && (VEC || col + 1 < S);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) {
+          const double g = s_g[j + m * s];
+          double x = 0.0, y = 0.0;
+          if (VEC) {
+            if (ok) {
+              const double2 u = __ldcs(reinterpret_cast<const double2*>(q + m * step));
+              x = u.x;
+              y = u.y;
+            }
+          } else {
+            if (okx) x = __ldcs(q + m * step);
+            if (oky) y = __ldcs(q + m * step + 1);
+          }
+          v[m] = make_double2(g * x, g * y);
+        }
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(kN2, RM);
+        if (!(fullp || pl0 + c < Pc)) return;
+        double2* q = Y + ((long long)t1 * kN2 + j) * Pc + pl0 + c;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) __stcg(q + (long long)m * s * Pc, cmul(w[m], s_twr[j + m * s]));
+      });
+}
+
+// ---------------------------------------------------------------------------------------------
+// forward stage 2: for the pair of residues (n2, N2-n2) (blockIdx.y = n2 in [0, N2/2]): N1-point FFTs over
+// t1 of Y[t1][n2][.], then separation of the two real columns on the half spectrum rows n <= Nt/2.
+// Sequences c in [0, 2P): c < P -> residue n2, pair c;  c >= P -> residue n2' = (N2-n2)%N2, pair c-P.
+// ---------------------------------------------------------------------------------------------
+template <int NT, int RM = 16>
+__global__ void __launch_bounds__(2 * kP * (NT / kN2) / elems_per_thread(NT / kN2, RM))
+tf4_fwd_s2(const double2* __restrict__ Y, long long S, long long p_begin, long long npairs_chunk,
+           double2* __restrict__ Sh, const double2* __restrict__ tw1) {
+  constexpr int N1 = NT / kN2, C = 2 * kP, NTH = C * N1 / elems_per_thread(N1, RM);
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw1[N1];
+  const int n2 = blockIdx.y, n2p = (kN2 - n2) % kN2;
+  const long long pl0 = (long long)blockIdx.x * kP;
+  const long long p0 = p_begin + pl0;
+  const long long Pc = npairs_chunk;
+  load_table(s_tw1, tw1, N1);
+  __syncthreads();
+  const bool fullp = pl0 + kP <= Pc;
+  fft_io<N1, C, false, false, NTH, false, true, RM>(
+      sm, s_tw1,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(N1, RM);
+        const int rr = c < kP ? n2 : n2p, pc = c & (kP - 1);
+        const bool ok = fullp || pl0 + pc < Pc;
+        const double2* q = Y + ((long long)j * kN2 + rr) * Pc + pl0 + pc;
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = ok ? __ldcg(q + (long long)m * s * kN2 * Pc) : czero();
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(N1, RM);
+        const int a = lin<N1, C, false>(j, c);
+#pragma unroll
+        for (int m = 0; m < RL; ++m) sm[soff<s * C>(a, m)] = w[m];
+      });
+  __syncthreads();
+  // outputs: rows n = rr + N2 n1 <= Nt/2 for rr in {n2, n2'} (each once), 2P real columns per row
+  const int nsets = (n2p == n2) ? 1 : 2;
+  const int total = nsets * N1 * 2 * kP;
+  for (int o = threadIdx.x; o < total; o += NTH) {
+    const int col = o % (2 * kP);
+    const int rowi = o / (2 * kP);          // [0, nsets*N1)
+    const int set = rowi / N1, n1 = rowi % N1;
+    const int rr = set == 0 ? n2 : n2p;
+    const int n = rr + kN2 * n1;
+    if (n > NT / 2) continue;
+    // partner index Nt - n = rr' + N2 n1'
+    const int m = (NT - n) & (NT - 1);
+    const int rrp = m % kN2, n1p = m / kN2;
+    const int pc = col >> 1;
+    const int cs = (rr == n2 ? 0 : kP) + pc;
+    const int cp = (rrp == n2 ? 0 : kP) + pc;
+    const double2 z1 = sm[sidx<N1, C, false>(n1, cs)];
+    const double2 z2 = sm[sidx<N1, C, false>(n1p, cp)];
+    double2 v;
+    if (col & 1)
+      v = make_double2(0.5 * (z1.y + z2.y), -0.5 * (z1.x - z2.x));
+    else
+      v = make_double2(0.5 * (z1.x + z2.x), 0.5 * (z1.y - z2.y));
+    const long long gcol = 2 * p0 + col;
+    if (pl0 + pc < Pc && gcol < S) __stcs(Sh + (long long)n * S + gcol, v);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// inverse stage 1: for residues (n2, N2-n2): rebuild Z[n] = X[n] + i Y[n] from the half spectrum, N1-point
+// inverse FFTs over n1, times w_Nt^{-t1 n2}; writes W[n2][t1][pl].
+// ---------------------------------------------------------------------------------------------
+template <int NT, int RM = 16>
+__global__ void __launch_bounds__(2 * kP * (NT / kN2) / elems_per_thread(NT / kN2, RM))
+tf4_inv_s1(const double2* __restrict__ Sh, long long S, long long p_begin, long long npairs_chunk,
+           double2* __restrict__ W, const double2* __restrict__ tw1, const double2* __restrict__ twt) {
+  constexpr int N1 = NT / kN2, C = 2 * kP, NTH = C * N1 / elems_per_thread(N1, RM);
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw1[N1], s_twa[N1], s_twb[N1];  // N1 twiddles; w_Nt^{-t1 n2}, w_Nt^{-t1 n2'}
+  const int n2 = blockIdx.y, n2p = (kN2 - n2) % kN2;
+  const long long pl0 = (long long)blockIdx.x * kP;
+  const long long p0 = p_begin + pl0;
+  const long long Pc = npairs_chunk;
+  for (int i = threadIdx.x; i < N1; i += NTH) {
+    s_tw1[i] = __ldg(tw1 + i);
+    s_twa[i] = cconj(__ldg(twt + i * n2));
+    s_twb[i] = cconj(__ldg(twt + i * n2p));
+  }
+  // stage the half-spectrum rows n <= Nt/2 with n % N2 in {n2, n2'}: slot (set, n1) -> 2P complex
+  const int nsets = (n2p == n2) ? 1 : 2;
+  const int total = nsets * N1 * 2 * kP;
+  for (int o = threadIdx.x; o < total; o += NTH) {
+    const int col = o % (2 * kP);
+    const int rowi = o / (2 * kP);
+    const int set = rowi / N1, n1 = rowi % N1;
+    const int n = (set == 0 ? n2 : n2p) + kN2 * n1;
+    const long long gcol = 2 * p0 + col;
+    double2 v = czero();
+    if (n <= NT / 2 && pl0 + (col >> 1) < Pc && gcol < S) v = __ldcs(Sh + (long long)n * S + gcol);
+    sm[pad(o)] = v;
+  }
+  __syncthreads();
+  const bool fullp = pl0 + kP <= Pc;
+  fft_io<N1, C, true, false, NTH, true, false, RM>(
+      sm, s_tw1,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(N1, RM);
+        const int rr = c < kP ? n2 : n2p, pc = c & (kP - 1);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) {
+          const int n1 = j + m * s;
+          const int n = rr + kN2 * n1;
+          const bool lo = n <= NT / 2;
+          const int mm = lo ? n : NT - n;  // row held in smem (<= Nt/2)
+          const int slot = ((mm % kN2) == n2 ? 0 : 1) * N1 + mm / kN2;
+          const double sg = lo ? 1.0 : -1.0;
+          const int base = slot * 2 * kP + 2 * pc;
+          const double2 X = sm[pad(base)], Yv = sm[pad(base + 1)];
+          v[m] = make_double2(fma(-sg, Yv.y, X.x), fma(sg, X.y, Yv.x));
+        }
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(N1, RM);
+        const int rr = c < kP ? n2 : n2p, pc = c & (kP - 1);
+        if (c >= kP && nsets == 1) return;  // duplicate of the self-partnered residue
+        if (!(fullp || pl0 + pc < Pc)) return;
+        const double2* tws = c < kP ? s_twa : s_twb;
+        double2* q = W + ((long long)rr * N1 + j) * Pc + pl0 + pc;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) __stcg(q + (long long)m * s * Pc, cmul(w[m], tws[j + m * s]));
+      });
+}
+
+// ---------------------------------------------------------------------------------------------
+// inverse stage 2: for fixed t1 (blockIdx.y): N2-point inverse FFT over n2 of W[n2][t1][.], outputs
+// t = t1 + N1 t2 scaled by Gamma^{-1}_t / Nt into the two real columns of each pair (MODE 1: +=).
+// ---------------------------------------------------------------------------------------------
+template <int NT, bool VEC, int MODE, int RM = 16>
+__global__ void __launch_bounds__(kP * kN2 / RM) tf4_inv_s2(const double2* __restrict__ W, long long S, long long p_begin,
+                                                           long long npairs_chunk, double* __restrict__ z,
+                                                           const double* __restrict__ igam,
+                                                           const double2* __restrict__ tw2) {
+  constexpr int N1 = NT / kN2, C = kP, NTH = kP * kN2 / RM;
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw2[kN2];
+  __shared__ double s_g[kN2];  // Gamma^{-1} / Nt of rows t1 + N1 t2
+  const int t1 = blockIdx.y;
+  const long long pl0 = (long long)blockIdx.x * kP;
+  const long long p0 = p_begin + pl0;
+  const long long Pc = npairs_chunk;
+  for (int i = threadIdx.x; i < kN2; i += NTH) {
+    s_tw2[i] = __ldg(tw2 + i);
+    s_g[i] = __ldg(igam + t1 + N1 * i) * (1.0 / NT);
+  }
+  __syncthreads();
+  const bool fullp = pl0 + kP <= Pc;
+  fft_io<kN2, C, true, false, NTH, false, false, RM>(
+      sm, s_tw2,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(kN2, RM);
+        const bool ok = fullp || pl0 + c < Pc;
+        const double2* q = W + ((long long)j * N1 + t1) * Pc + pl0 + c;
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = ok ? __ldcg(q + (long long)m * s * N1 * Pc) : czero();
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(kN2, RM);
+        if (!(fullp || pl0 + c < Pc)) return;
+        const long long col = 2 * (p0 + c);
+        double* q = z + (long long)(t1 + N1 * j) * S + col;
+        const long long step = (long long)N1 * s * S;
+        const bool okx = VEC || col < S, oky = VEC || col + 1 < S;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) {
+          const double g = s_g[j + m * s];
+          double* row = q + m * step;
+          if (VEC) {
+            double2* rp = reinterpret_cast<double2*>(row);
+            if (MODE) {
+              const double2 o = *rp;
+              *rp = make_double2(fma(g, w[m].x, o.x), fma(g, w[m].y, o.y));
+            } else {
+              __stcs(rp, make_double2(g * w[m].x, g * w[m].y));
+            }
+          } else {
+            if (okx) row[0] = MODE ? fma(g, w[m].x, row[0]) : g * w[m].x;
+            if (oky) row[1] = MODE ? fma(g, w[m].y, row[1]) : g * w[m].y;
+          }
+        }
+      });
+}
+
+template <int N>
+int smem_of(int C) {
+  return smem_elems(N * C) * (int)sizeof(double2);
+}
+
+// non-persistent grid versions: one CTA per tile
+template <int NT, int RM>
+void fwd_grid(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
+              double2* scratch, long long p, long long pc, bool vec, cudaStream_t st) {
+  constexpr int N1 = NT / kN2;
+  const int sm1 = smem_of<kN2>(kP), sm2 = smem_of<N1>(2 * kP);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tf4_fwd_s1<NT, true, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_fwd_s1<NT, false, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_fwd_s2<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    attr = true;
+  }
+  const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
+  const dim3 g1(nt1, N1), g2(nt1, kN2 / 2 + 1);
+  if (vec)
+    tf4_fwd_s1<NT, true, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+  else
+    tf4_fwd_s1<NT, false, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+  tf4_fwd_s2<NT, RM><<<g2, 2 * kP * N1 / elems_per_thread(N1, RM), sm2, st>>>(scratch, S, p, pc, Sh, tb.tw1);
+}
+
+template <int NT, int RM>
+void inv_grid(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
+              double2* scratch, long long p, long long pc, int accumulate, bool vec, cudaStream_t st) {
+  constexpr int N1 = NT / kN2;
+  const int sm1 = smem_of<N1>(2 * kP) > smem_elems(2 * N1 * 2 * kP) * (int)sizeof(double2)
+                      ? smem_of<N1>(2 * kP)
+                      : smem_elems(2 * N1 * 2 * kP) * (int)sizeof(double2);
+  const int sm2 = smem_of<kN2>(kP);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tf4_inv_s1<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, true, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, true, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, false, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, false, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    attr = true;
+  }
+  const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
+  const dim3 g1(nt1, kN2 / 2 + 1), g2(nt1, N1);
+  tf4_inv_s1<NT, RM><<<g1, 2 * kP * N1 / elems_per_thread(N1, RM), sm1, st>>>(Sh, S, p, pc, scratch, tb.tw1, tb.twt);
+  const int th2 = kP * kN2 / RM;
+  if (vec) {
+    if (accumulate)
+      tf4_inv_s2<NT, true, 1, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+    else
+      tf4_inv_s2<NT, true, 0, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+  } else {
+    if (accumulate)
+      tf4_inv_s2<NT, false, 1, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+    else
+      tf4_inv_s2<NT, false, 0, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+  }
+}
+
+constexpr int kRmaxGrid = 8;  // radix-8 passes: 8 elements per thread, twice the warps of radix 16 (measured faster)
+
+template <int NT>
+cudaError_t fwd_n(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
+                  double2* scratch, long long chunk_pairs, cudaStream_t st, int* nl) {
+  const bool vec = (S % 2 == 0) && ((reinterpret_cast<uintptr_t>(r) & 15) == 0);
+  const long long npairs = (S + 1) / 2;
+  int n = 0;
+  for (long long p = 0; p < npairs; p += chunk_pairs) {
+    const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
+    fwd_grid<NT, kRmaxGrid>(r, Sh, S, gam, tb, scratch, p, pc, vec, st);
+    n += 2;
+  }
+  *nl = n;
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t inv_n(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
+                  double2* scratch, long long chunk_pairs, int accumulate, cudaStream_t st, int* nl) {
+  const bool vec = (S % 2 == 0) && ((reinterpret_cast<uintptr_t>(z) & 15) == 0);
+  const long long npairs = (S + 1) / 2;
+  int n = 0;
+  for (long long p = 0; p < npairs; p += chunk_pairs) {
+    const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
+    inv_grid<NT, kRmaxGrid>(Sh, z, S, igam, tb, scratch, p, pc, accumulate, vec, st);
+    n += 2;
+  }
+  *nl = n;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int pd_tf4_supported(int nt) { return nt == 1024 || nt == 2048 || nt == 4096; }
+int pd_tf4_n2() { return kN2; }
+int pd_tf4_pairs_per_tile() { return kP; }
+
+cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+                              const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
+                              int* nl) {
+  switch (nt) {
+    case 1024: return fwd_n<1024>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
+    case 2048: return fwd_n<2048>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
+    case 4096: return fwd_n<4096>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
+    case 8192: return fwd_n<8192>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t pd_launch_tf4_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+                              const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, int accumulate,
+                              cudaStream_t st, int* nl) {
+  switch (nt) {
+    case 1024: return inv_n<1024>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
+    case 2048: return inv_n<2048>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
+    case 4096: return inv_n<4096>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
+    case 8192: return inv_n<8192>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
+    default: return cudaErrorInvalidValue;
+  }
+}
