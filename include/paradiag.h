@@ -64,9 +64,17 @@ typedef struct {
   double nu, ax, ay;
 } pd_grid;
 
+/* Distribution: rank p owns the spatial slab of pd_partition() for all Nt levels (1D: an
+ * x-range, 2D: a range of y-rows); Step (b) runs on frequency shards after an all-to-all over NCCL.
+ *   size == 1              single GPU (rank must be 0, nccl_id ignored)
+ *   size > 1, rank >= 0    NCCL rank `rank` of `size`; vectors passed to the context are the LOCAL slab
+ *                          [Nt][S_local] (pd_local_shape); nccl_id from pd_nccl_unique_id on one rank
+ *   size > 1, rank < 0     `size` virtual ranks inside this process on one GPU: vectors are GLOBAL, every
+ *                          exchange of the plan is executed with device copies (test mode of the sharded
+ *                          path; same plan, partition and kernels as the NCCL mode) */
 typedef struct {
-  int rank, size;               /* size == 1 => single GPU (nccl_id ignored) */
-  const void* nccl_id;          /* 128-byte ncclUniqueId shared by all ranks (from pd_nccl_unique_id) */
+  int rank, size;
+  const void* nccl_id;          /* 128-byte ncclUniqueId shared by all ranks */
 } pd_dist;
 
 typedef struct {
@@ -92,6 +100,11 @@ PD_API const char* pd_last_error(const pd_ctx* ctx);
 
 /* The 128-byte NCCL unique id for a multi-GPU setup (rank 0 creates it and broadcasts it). */
 PD_API pd_status pd_nccl_unique_id(void* out128);
+
+/* Partition plan (pure host, no GPU): for each of `size` ranks the spatial slab [s_off, s_off + s_cnt) in
+ * dofs and the half-spectrum frequency range [f_off, f_off + f_cnt).  Arrays of length size (nullable). */
+PD_API pd_status pd_partition(int op, int nx, int ny, int nt, int size, long long* s_off, long long* s_cnt,
+                              int* f_off, int* f_cnt);
 
 /* Local slab of this rank: 1D x-range [offset, offset+nx_local), 2D y-rows [offset/nx, ...). */
 PD_API pd_status pd_local_shape(const pd_ctx* ctx, int* nx_local, int* ny_local, long long* offset);

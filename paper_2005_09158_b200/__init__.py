@@ -18,7 +18,8 @@ from ._lib import (  # noqa: F401
     exported_symbols,
     load_library,
     nccl_unique_id,
+    partition,
 )
 
-__all__ = ["ParaDiag", "ParaDiagError", "Report", "load_library", "exported_symbols", "nccl_unique_id",
+__all__ = ["ParaDiag", "ParaDiagError", "Report", "load_library", "exported_symbols", "nccl_unique_id", "partition",
            "ADE1D_DIRICHLET", "WAVE1D_DIRICHLET", "ADE2D_PERIODIC", "BE", "CN", "LEAPFROG"]

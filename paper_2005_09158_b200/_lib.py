@@ -81,6 +81,8 @@ def load_library(path: str | None = None):
         "pd_kernel_launches": (C.c_longlong, [vp]),
         "pd_enable_phase_timing": (ip, [vp, ip]),
         "pd_phase_times": (ip, [vp, dp, C.POINTER(C.c_longlong)]),
+        "pd_partition": (ip, [ip, ip, ip, ip, ip, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                              C.POINTER(ip), C.POINTER(ip)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -116,6 +118,15 @@ def _check(lib, ctx, st: int, allow=(PD_OK,)):
     return st
 
 
+def partition(op: int, nx: int, ny: int, nt: int, size: int):
+    """Partition plan of the sharded path (pure host): lists s_off, s_cnt, f_off, f_cnt over ranks."""
+    lib = load_library()
+    so, sc = (C.c_longlong * size)(), (C.c_longlong * size)()
+    fo, fc = (C.c_int * size)(), (C.c_int * size)()
+    _check(lib, None, lib.pd_partition(op, nx, ny, nt, size, so, sc, fo, fc))
+    return list(so), list(sc), list(fo), list(fc)
+
+
 def nccl_unique_id() -> bytes:
     lib = load_library()
     buf = C.create_string_buffer(128)
@@ -137,6 +148,7 @@ class ParaDiag:
 
     op: ADE1D_DIRICHLET | WAVE1D_DIRICHLET | ADE2D_PERIODIC;  scheme: BE | CN | LEAPFROG.
     Vectors are CUDA float64 tensors of shape [Nt, S_local] (S = nx*ny spatial dofs of this rank).
+    rank=-1 with size>1 runs `size` virtual ranks of the sharded path on this GPU (global vectors).
     """
 
     def __init__(self, op: int, nx: int, ny: int, length: float, nu: float, ax: float, ay: float,
@@ -150,6 +162,7 @@ class ParaDiag:
         g = pd_grid(op, nx, ny, length, nu, ax, ay)
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = pd_dist(rank, size, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
+        self.rank, self.size = rank, size
         ctx = C.c_void_p()
         st = self._lib.pd_setup(C.byref(g), dt, nt, alpha, scheme, C.byref(d),
                                 C.c_void_p(self.stream.cuda_stream), C.byref(ctx))

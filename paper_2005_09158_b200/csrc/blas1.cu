@@ -22,7 +22,6 @@ struct PtrPack {
   double c[kMaxK];
 };
 
-PD_D double2 ld2(const double* p, long long i) { return __ldcs(reinterpret_cast<const double2*>(p) + i); }
 PD_D double2 ld2_keep(const double* p, long long i) { return __ldg(reinterpret_cast<const double2*>(p) + i); }
 
 // deterministic block reduction of K values per thread -> partial[blockIdx.x * K + i]

@@ -1,0 +1,131 @@
+// Context of the ParaDiag-II library (shared by paradiag.cpp and dist.cpp; not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <complex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/paradiag.h"
+#include "comm.h"
+#include "kernels.h"
+
+// partition plan: spatial slabs (1D x-ranges, 2D y-row ranges, in dofs) and frequency ranges per rank
+struct pd_plan {
+  int P = 1;
+  std::vector<long long> s_off, s_cnt;  // spatial dofs
+  std::vector<int> f_off, f_cnt;        // half-spectrum frequencies
+  std::vector<int> e_off, e_cnt;        // extent units (1D: x, 2D: y rows)
+};
+pd_plan pd_make_plan(int op, int nx, int ny, int nt, int P);
+
+// per-rank state of the sharded path
+struct pd_shard {
+  int rank = 0;
+  long long S = 0, off = 0;   // local spatial dofs and first global dof
+  int ext = 0, ext_off = 0;   // local extent (1D: x points, 2D: y rows) and its global start
+  int F = 0, f0 = 0;          // local frequencies
+  double2* Sh_loc = nullptr;  // [F_all][S]  all frequencies of the local slab
+  double2* Sg = nullptr;      // [F][S_glob] local frequencies of every spatial dof
+  double2* stage = nullptr;   // NCCL receive/send staging
+  double* hlo = nullptr;      // halos [Nt][hw]
+  double* hhi = nullptr;
+  double* h1lo = nullptr;     // single-level halos for the rhs (u0, v0): [2][hw]
+  double* h1hi = nullptr;
+  double* sendlo = nullptr;   // NCCL halo send buffers [Nt][hw]
+  double* sendhi = nullptr;
+  double* r_loc = nullptr;    // mode 2: local copies of in/out vectors [Nt][S]
+  double* z_loc = nullptr;
+  double* b_loc = nullptr;
+  pd_stencil sten{};          // local stencil parameters
+};
+
+struct pd_ctx {
+  // problem
+  pd_grid g{};
+  double dt = 0, alpha = 0;
+  int nt = 0, F = 0;
+  pd_scheme scheme = PD_BE;
+  cudaStream_t st = nullptr;
+  // distribution: mode 0 single GPU; 1 NCCL rank of `size` (local vectors); 2 `size` virtual ranks in this
+  // process on one GPU (global vectors, exchanges by device copies; test mode for the sharded path)
+  int rank = 0, size = 1, dist_mode = 0;
+  pd_comm* comm = nullptr;
+  std::vector<pd_shard> shards;  // modes 1 (one entry: this rank) and 2 (all virtual ranks)
+  pd_plan plan;
+  int nx_loc = 0, ny_loc = 0;    // local spatial extent (1D: x-range, 2D: y-rows)
+  long long off = 0;             // first local spatial dof (global index)
+  long long S = 0;               // local spatial dofs
+  long long Sg = 0;              // global spatial dofs
+  // tables (device)
+  double* gam = nullptr;
+  double* igam = nullptr;
+  double2* tw_t = nullptr;       // exp(-2 pi i j / Nt)
+  double2* tw_n1 = nullptr;      // four-step tables (Nt >= 1024)
+  double2* tw_n2 = nullptr;
+  double2* tf4_scratch = nullptr;
+  long long tf4_chunk = 0;
+  bool use_tf4 = false;
+  double2* lam1 = nullptr;       // half spectrum, F entries
+  double2* lam2 = nullptr;
+  pd_tri_coef* tri = nullptr;    // 1D
+  double* sx = nullptr;          // 2D: sin^2(pi k / N)
+  double* sn = nullptr;          // 2D: sin(2 pi k / N)
+  double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
+  pd_slab_params slab{};
+  int slab_chunk = 1;
+  pd_stencil sten{};
+  // host copies
+  std::vector<std::complex<double>> lam1_full, lam2_full;
+  // workspace
+  double2* Sh = nullptr;         // half spectrum [F][S] complex (frequency-sharded layout when size > 1)
+  double* rvec = nullptr;        // residual / temp vector
+  double* partial = nullptr;     // reduction partials
+  int npartial = 0;
+  double* dred = nullptr;        // reduced scalars (device)
+  double* hred = nullptr;        // pinned host scalars
+  // GMRES
+  int gm_m = 0;
+  std::vector<double*> V;
+  double* zvec = nullptr;
+  // host-buffer staging
+  double* stage_a = nullptr;
+  double* stage_b = nullptr;
+  // diagnostics
+  long long launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> evpool;          // recorded pairs, resolved lazily (no sync per phase)
+  std::vector<std::pair<int, int>> evrec;   // (phase, index of begin event)
+  int ev_open[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  double phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long phase_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::string err;
+};
+
+
+pd_status fail(pd_ctx* c, pd_status s, const char* fmt, ...);
+
+#define PD_CUDA(ctx, expr)                                                                    \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, PD_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define PD_LAUNCH(ctx, expr) \
+  do {                       \
+    PD_CUDA(ctx, expr);      \
+    (ctx)->launches++;       \
+  } while (0)
+
+// dist.cpp
+pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id);
+void pd_dist_free(pd_ctx* c);
+pd_status pd_dist_apply(pd_ctx* c, const double* r, double* z, int accumulate);
+pd_status pd_dist_stencil(pd_ctx* c, const double* b, const double* u, double* out, double* norm2_dev_partial_sum);
+pd_status pd_dist_build_rhs(pd_ctx* c, const double* u0, const double* v0, const double* f, double* b);
+// paradiag.cpp helpers used by dist.cpp
+pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0);
+pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S);
+pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate);

@@ -64,6 +64,11 @@ struct pd_stencil {
   double k2c, k2x_m, k2x_p, k2y_m, k2y_p;  // 2D K stencil: centre, x-1, x+1, y-1, y+1
   double dt;
   double theta;
+  // halos of the sharded path (NULL: 1D zero Dirichlet boundary, 2D periodic wrap within the local rows).
+  // Stencil: [Nt][hw] (hw = 1 in 1D, N in 2D) = the neighbour's boundary column/row at every time level;
+  // rhs: [2][hw] = neighbour values of U_0 (row 0) and V_0 (row 1).
+  const double* hlo;
+  const double* hhi;
 };
 // out = b - A u (b != NULL) or out = A u (b == NULL); per-block partial sums of out^2 into partial[]
 cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double* u, double* out, double* partial,

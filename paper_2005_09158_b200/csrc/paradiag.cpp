@@ -16,74 +16,13 @@
 #include <string>
 #include <vector>
 
-#include "../../include/paradiag.h"
-#include "comm.h"
-#include "kernels.h"
+#include "ctx.h"
 
 typedef std::complex<long double> cld;
 
-struct pd_ctx {
-  // problem
-  pd_grid g{};
-  double dt = 0, alpha = 0;
-  int nt = 0, F = 0;
-  pd_scheme scheme = PD_BE;
-  cudaStream_t st = nullptr;
-  // distribution
-  int rank = 0, size = 1;
-  pd_comm* comm = nullptr;
-  int nx_loc = 0, ny_loc = 0;    // local spatial extent (1D: x-range, 2D: y-rows)
-  long long off = 0;             // first local spatial dof (global index)
-  long long S = 0;               // local spatial dofs
-  long long Sg = 0;              // global spatial dofs
-  // tables (device)
-  double* gam = nullptr;
-  double* igam = nullptr;
-  double2* tw_t = nullptr;       // exp(-2 pi i j / Nt)
-  double2* tw_n1 = nullptr;      // four-step tables (Nt >= 1024)
-  double2* tw_n2 = nullptr;
-  double2* tf4_scratch = nullptr;
-  long long tf4_chunk = 0;
-  bool use_tf4 = false;
-  double2* lam1 = nullptr;       // half spectrum, F entries
-  double2* lam2 = nullptr;
-  pd_tri_coef* tri = nullptr;    // 1D
-  double* sx = nullptr;          // 2D: sin^2(pi k / N)
-  double* sn = nullptr;          // 2D: sin(2 pi k / N)
-  double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
-  pd_slab_params slab{};
-  int slab_chunk = 1;
-  pd_stencil sten{};
-  // host copies
-  std::vector<std::complex<double>> lam1_full, lam2_full;
-  // workspace
-  double2* Sh = nullptr;         // half spectrum [F][S] complex (frequency-sharded layout when size > 1)
-  double* rvec = nullptr;        // residual / temp vector
-  double* partial = nullptr;     // reduction partials
-  int npartial = 0;
-  double* dred = nullptr;        // reduced scalars (device)
-  double* hred = nullptr;        // pinned host scalars
-  // GMRES
-  int gm_m = 0;
-  std::vector<double*> V;
-  double* zvec = nullptr;
-  // host-buffer staging
-  double* stage_a = nullptr;
-  double* stage_b = nullptr;
-  // diagnostics
-  long long launches = 0;
-  bool timing = false;
-  std::vector<cudaEvent_t> evpool;          // recorded pairs, resolved lazily (no sync per phase)
-  std::vector<std::pair<int, int>> evrec;   // (phase, index of begin event)
-  int ev_open[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
-  double phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long phase_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  std::string err;
-};
-
 static thread_local std::string g_setup_err;
 
-static pd_status fail(pd_ctx* c, pd_status s, const char* fmt, ...) {
+pd_status fail(pd_ctx* c, pd_status s, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -95,19 +34,6 @@ static pd_status fail(pd_ctx* c, pd_status s, const char* fmt, ...) {
     g_setup_err = buf;
   return s;
 }
-
-#define PD_CUDA(ctx, expr)                                                                    \
-  do {                                                                                        \
-    cudaError_t e_ = (expr);                                                                  \
-    if (e_ != cudaSuccess)                                                                    \
-      return fail(ctx, PD_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-
-#define PD_LAUNCH(ctx, expr) \
-  do {                       \
-    PD_CUDA(ctx, expr);      \
-    (ctx)->launches++;       \
-  } while (0)
 
 template <class T>
 static cudaError_t dalloc(T** p, size_t n) {
@@ -203,6 +129,7 @@ static void free_ctx(pd_ctx* c) {
     if (p) cudaFree(p);
   for (double* p : c->V) cudaFree(p);
   if (c->hred) cudaFreeHost(c->hred);
+  pd_dist_free(c);
   for (auto& e : c->evpool)
     if (e) cudaEventDestroy(e);
   if (c->comm) pd_comm_destroy(c->comm);
@@ -245,7 +172,7 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     return fail(nullptr, PD_EINVAL, "unknown operator %d", (int)g->op);
   }
   const int size = dist ? dist->size : 1, rank = dist ? dist->rank : 0;
-  if (size < 1 || rank < 0 || rank >= size) return fail(nullptr, PD_EINVAL, "bad rank/size %d/%d", rank, size);
+  if (size < 1 || rank >= size || (size == 1 && rank != 0)) return fail(nullptr, PD_EINVAL, "bad rank/size %d/%d", rank, size);
 
   pd_ctx* c = new pd_ctx();
   c->g = *g;
@@ -255,39 +182,29 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   c->alpha = alpha;
   c->scheme = s;
   c->st = (cudaStream_t)cuda_stream;
-  c->rank = rank;
+  c->rank = rank < 0 ? 0 : rank;
   c->size = size;
   c->Sg = (long long)g->nx * g->ny;
 
   // ---- distribution: spatial slabs (1D: x-ranges, 2D: y-row ranges) ----
-  {
-    const int ext = g->op == PD_ADE2D_PERIODIC ? g->ny : g->nx;
-    const int base = ext / size, rem = ext % size;
-    const int lo = rank * base + (rank < rem ? rank : rem);
-    const int cnt = base + (rank < rem ? 1 : 0);
-    if (g->op == PD_ADE2D_PERIODIC) {
-      c->nx_loc = g->nx;
-      c->ny_loc = cnt;
-      c->off = (long long)lo * g->nx;
-    } else {
-      c->nx_loc = cnt;
-      c->ny_loc = 1;
-      c->off = lo;
-    }
-    c->S = (long long)c->nx_loc * c->ny_loc;
+  // dist == NULL or size == 1: single GPU.  rank >= 0: NCCL rank (local slab vectors).  rank < 0: `size`
+  // virtual ranks in this process on one GPU (global vectors; the sharded path's test mode).
+  c->dist_mode = size > 1 ? (dist->rank < 0 ? 2 : 1) : 0;
+  if (c->dist_mode == 1 && !dist->nccl_id) {
+    free_ctx(c);
+    return fail(nullptr, PD_EINVAL, "multi-GPU setup needs an NCCL unique id (pd_nccl_unique_id)");
   }
-  if (size > 1) {
-    if (!dist->nccl_id) {
-      free_ctx(c);
-      return fail(nullptr, PD_EINVAL, "multi-GPU setup needs an NCCL unique id");
-    }
-    c->comm = pd_comm_create(dist->nccl_id, rank, size, c->st);
-    if (!c->comm) {
-      std::string m = pd_comm_last_error();
-      free_ctx(c);
-      return fail(nullptr, PD_ENCCL, "NCCL init failed: %s", m.c_str());
-    }
-    // the distributed apply (transposes) lives in comm.cpp
+  if (c->dist_mode == 1) {
+    const pd_plan pl = pd_make_plan(g->op, g->nx, g->ny, nt, size);
+    c->off = pl.s_off[rank];
+    c->S = pl.s_cnt[rank];
+    c->nx_loc = g->op == PD_ADE2D_PERIODIC ? g->nx : pl.e_cnt[rank];
+    c->ny_loc = g->op == PD_ADE2D_PERIODIC ? pl.e_cnt[rank] : 1;
+  } else {
+    c->nx_loc = g->nx;
+    c->ny_loc = g->ny;
+    c->off = 0;
+    c->S = c->Sg;
   }
 
   // ---- spectra, Gamma, twiddles ----
@@ -446,6 +363,20 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   SETUP_CUDA(dalloc(&c->partial, (size_t)c->npartial));
   SETUP_CUDA(dalloc(&c->dred, 64));
   SETUP_CUDA(cudaMallocHost((void**)&c->hred, 64 * sizeof(double)));
+  if (c->dist_mode != 0) {
+    // partials of every shard's stencil launch live side by side
+    if (c->dist_mode == 2) {
+      cudaFree(c->partial);
+      c->npartial *= size;
+      SETUP_CUDA(dalloc(&c->partial, (size_t)c->npartial));
+    }
+    const pd_status ds = pd_dist_setup(c, dist->nccl_id);
+    if (ds != PD_OK) {
+      std::string m = c->err;
+      free_ctx(c);
+      return fail(nullptr, ds, "%s", m.c_str());
+    }
+  }
 #undef SETUP_CUDA
   *out = c;
   return PD_OK;
@@ -537,8 +468,9 @@ static void phase_end(pd_ctx* c, int ph) {
   }
 }
 
-// Step (b) on the workspace spectrum (local frequencies: all F when size == 1)
-static pd_status spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
+// Step (b) on a spectrum buffer holding frequencies [f0, f0 + nfreq) on full spatial rows
+pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
+  phase_begin(c, 1);
   if (c->g.op == PD_ADE2D_PERIODIC) {
     int nl = 0;
     PD_CUDA(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
@@ -547,64 +479,67 @@ static pd_status spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   } else {
     PD_LAUNCH(c, pd_launch_tridiag(Sh, c->g.nx, nfreq, c->tri + f0, pd_tridiag_rows_per_thread(), c->st));
   }
+  phase_end(c, 1);
   return PD_OK;
 }
 
-// z = P^{-1} r, or u += P^{-1} r when accumulate
-static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
-  if (c->size > 1) {
-    return pd_comm_apply(c->comm, c, r, z, accumulate) == 0 ? PD_OK
-                                                            : fail(c, PD_ENCCL, "distributed apply: %s", pd_comm_last_error());
-  }
+// Step (a) of a local slab: r [Nt][S] -> Sh [F][S]
+pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) {
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   phase_begin(c, 0);
   if (c->use_tf4) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, c->Sh, c->S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
+    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, Sh, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
     c->launches += nl;
   } else {
-    PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, c->Sh, c->S, c->gam, c->tw_t, c->st));
+    PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, Sh, S, c->gam, c->tw_t, c->st));
   }
   phase_end(c, 0);
-  phase_begin(c, 1);
-  pd_status s = spatial_solve(c, c->Sh, c->F, 0);
-  if (s != PD_OK) return s;
-  phase_end(c, 1);
+  return PD_OK;
+}
+
+// Step (c) of a local slab: Sh [F][S] -> z [Nt][S] (z += when accumulate)
+pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate) {
+  const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   const int ph = accumulate ? 4 : 2;
   phase_begin(c, ph);
   if (c->use_tf4) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tf4_inv(c->nt, c->Sh, z, c->S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate,
-                                 c->st, &nl));
+    PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl));
     c->launches += nl;
   } else {
-    PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, c->Sh, z, c->S, c->igam, c->tw_t, accumulate, c->st));
+    PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, Sh, z, S, c->igam, c->tw_t, accumulate, c->st));
   }
   phase_end(c, ph);
   return PD_OK;
 }
 
+// z = P^{-1} r, or u += P^{-1} r when accumulate
+static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
+  if (c->dist_mode != 0) return pd_dist_apply(c, r, z, accumulate);
+  pd_status s = pd_time_fft_fwd(c, r, c->Sh, c->S);
+  if (s != PD_OK) return s;
+  s = pd_spatial_solve(c, c->Sh, c->F, 0);
+  if (s != PD_OK) return s;
+  return pd_time_fft_inv(c, c->Sh, z, c->S, accumulate);
+}
+
 // out = b - A u (b != NULL) or A u; if norm2 != NULL: deterministic ||out||^2 into *norm2 (host, syncs)
 static pd_status stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2) {
-  if (c->size > 1) {
-    if (pd_comm_halo_stencil(c->comm, c, b, u, out) != 0)
-      return fail(c, PD_ENCCL, "distributed residual: %s", pd_comm_last_error());
+  const int ph = b ? 3 : 5;
+  phase_begin(c, ph);
+  if (c->dist_mode != 0) {
+    pd_status s = pd_dist_stencil(c, b, u, out, nullptr);  // local sum of squares -> dred[0]
+    if (s != PD_OK) return s;
   } else {
     int nb = 0;
-    const int ph = b ? 3 : 5;
-    phase_begin(c, ph);
     PD_LAUNCH(c, pd_launch_stencil(c->sten, b, u, out, c->partial, &nb, c->st));
-    phase_end(c, ph);
-    if (norm2) {
-      PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, nb, 1, c->dred, c->st));
-    }
+    if (norm2) PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, nb, 1, c->dred, c->st));
   }
+  phase_end(c, ph);
   if (norm2) {
-    if (c->size > 1) {
-      // the distributed stencil leaves the local partial sum in dred[0]
-      if (pd_comm_allreduce_sum(c->comm, c->dred, 1) != 0)
-        return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
-    }
+    if (c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, 1) != 0)
+      return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
     PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     PD_CUDA(c, cudaStreamSynchronize(c->st));
     *norm2 = c->hred[0];
@@ -623,7 +558,7 @@ static pd_status krylov_impl(pd_ctx* c, int mode, const double* const* X, const 
     const int kk = mode == 2 ? 1 : k;
     PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), kk, c->dred, c->st));
     phase_end(c, 6);
-    if (c->size > 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
+    if (c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
       return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
     PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, kk * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     PD_CUDA(c, cudaStreamSynchronize(c->st));
@@ -658,11 +593,7 @@ pd_status pd_matvec(pd_ctx* c, const double* u, double* w) {
 
 pd_status pd_build_rhs(pd_ctx* c, const double* u0, const double* v0, const double* f, double* b) {
   if (!c || !u0 || !b) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
-  if (c->size > 1) {
-    if (pd_comm_build_rhs(c->comm, c, u0, v0, f, b) != 0)
-      return fail(c, PD_ENCCL, "distributed rhs: %s", pd_comm_last_error());
-    return PD_OK;
-  }
+  if (c->dist_mode != 0) return pd_dist_build_rhs(c, u0, v0, f, b);
   PD_LAUNCH(c, pd_launch_rhs(c->sten, u0, v0, f, b, c->st));
   return PD_OK;
 }
@@ -879,28 +810,3 @@ pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, dou
 
 }  // extern "C"
 
-// accessors used by comm.cpp (distributed apply)
-pd_ctx_view pd_ctx_get_view(pd_ctx* c) {
-  pd_ctx_view v;
-  v.nt = c->nt;
-  v.F = c->F;
-  v.op = c->g.op;
-  v.nx = c->g.nx;
-  v.ny = c->g.ny;
-  v.nx_loc = c->nx_loc;
-  v.ny_loc = c->ny_loc;
-  v.S = c->S;
-  v.Sg = c->Sg;
-  v.off = c->off;
-  v.st = c->st;
-  v.gam = c->gam;
-  v.igam = c->igam;
-  v.tw_t = c->tw_t;
-  v.sten = c->sten;
-  v.partial = c->partial;
-  v.dred = c->dred;
-  v.Sh = c->Sh;
-  return v;
-}
-int pd_ctx_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) { return spatial_solve(c, Sh, nfreq, f0) == PD_OK ? 0 : -1; }
-void pd_ctx_count_launch(pd_ctx* c, int n) { c->launches += n; }

@@ -35,11 +35,12 @@ PD_D Taps taps_of(const pd_stencil& p) {
 // ---------------- 1D: neighbourhood = (x-1, x, x+1) ----------------
 struct N1 { double l, c, r; };
 
-PD_D N1 load1(const double* __restrict__ row, int x, int nx) {
+// hl, hr: halo rows (neighbour values for x = -1 and x = nx) or NULL for the Dirichlet zero
+PD_D N1 load1(const double* __restrict__ row, int x, int nx, const double* hl, const double* hr) {
   N1 v;
   v.c = row[x];
-  v.l = x > 0 ? row[x - 1] : 0.0;
-  v.r = x + 1 < nx ? row[x + 1] : 0.0;
+  v.l = x > 0 ? row[x - 1] : (hl ? *hl : 0.0);
+  v.r = x + 1 < nx ? row[x + 1] : (hr ? *hr : 0.0);
   return v;
 }
 
@@ -53,15 +54,17 @@ __global__ void __launch_bounds__(kBX) stencil1d_kernel(pd_stencil p, const doub
   const bool act = x < nx;
   double acc = 0.0;
   N1 h1 = {0, 0, 0}, h2 = {0, 0, 0};  // rows n-1, n-2
+  const double* hl = p.hlo;
+  const double* hr = p.hhi;
   if (act) {
-    if (n0 - 1 >= 0) h1 = load1(u + (long long)(n0 - 1) * nx, x, nx);
-    if (n0 - 2 >= 0) h2 = load1(u + (long long)(n0 - 2) * nx, x, nx);
+    if (n0 - 1 >= 0) h1 = load1(u + (long long)(n0 - 1) * nx, x, nx, hl ? hl + n0 - 1 : nullptr, hr ? hr + n0 - 1 : nullptr);
+    if (n0 - 2 >= 0) h2 = load1(u + (long long)(n0 - 2) * nx, x, nx, hl ? hl + n0 - 2 : nullptr, hr ? hr + n0 - 2 : nullptr);
   }
   const int n1 = min(n0 + kTC, p.nt);
 #pragma unroll 8
   for (int n = n0; n < n1; ++n) {
     N1 h0 = {0, 0, 0};
-    if (act) h0 = load1(u + (long long)n * nx, x, nx);
+    if (act) h0 = load1(u + (long long)n * nx, x, nx, hl ? hl + n : nullptr, hr ? hr + n : nullptr);
     // y = sum_k c2_k u_{n-k}; Au = sum_k c1_k u_{n-k} + K y
     const double yl = tp.c2[0] * h0.l + tp.c2[1] * h1.l + tp.c2[2] * h2.l;
     const double yc = tp.c2[0] * h0.c + tp.c2[1] * h1.c + tp.c2[2] * h2.c;
@@ -92,15 +95,15 @@ __global__ void __launch_bounds__(kBX) stencil1d_kernel(pd_stencil p, const doub
 // ---------------- 2D periodic: neighbourhood = (c, x-1, x+1, y-1, y+1) ----------------
 struct N2 { double c, xm, xp, ym, yp; };
 
-PD_D N2 load2(const double* __restrict__ slab, int x, int y, int nx, int ny) {
+// hl, hr: halo rows for y = -1 and y = ny (neighbour ranks) or NULL for the periodic wrap within the slab
+PD_D N2 load2(const double* __restrict__ slab, int x, int y, int nx, int ny, const double* hl, const double* hr) {
   N2 v;
   const int xm = x == 0 ? nx - 1 : x - 1, xp = x == nx - 1 ? 0 : x + 1;
-  const int ym = y == 0 ? ny - 1 : y - 1, yp = y == ny - 1 ? 0 : y + 1;
   v.c = slab[(long long)y * nx + x];
   v.xm = slab[(long long)y * nx + xm];
   v.xp = slab[(long long)y * nx + xp];
-  v.ym = slab[(long long)ym * nx + x];
-  v.yp = slab[(long long)yp * nx + x];
+  v.ym = y > 0 ? slab[(long long)(y - 1) * nx + x] : (hl ? hl[x] : slab[(long long)(ny - 1) * nx + x]);
+  v.yp = y + 1 < ny ? slab[(long long)(y + 1) * nx + x] : (hr ? hr[x] : slab[x]);
   return v;
 }
 
@@ -116,15 +119,22 @@ __global__ void __launch_bounds__(kBX) stencil2d_kernel(pd_stencil p, const doub
   const int n0 = blockIdx.y * kTC;
   double acc = 0.0;
   N2 h1 = {0, 0, 0, 0, 0}, h2 = {0, 0, 0, 0, 0};
+  const double* hl = p.hlo;
+  const double* hr = p.hhi;
   if (act) {
-    if (n0 - 1 >= 0) h1 = load2(u + (n0 - 1) * S, x, y, nx, ny);
-    if (n0 - 2 >= 0) h2 = load2(u + (n0 - 2) * S, x, y, nx, ny);
+    if (n0 - 1 >= 0)
+      h1 = load2(u + (n0 - 1) * S, x, y, nx, ny, hl ? hl + (long long)(n0 - 1) * nx : nullptr,
+                 hr ? hr + (long long)(n0 - 1) * nx : nullptr);
+    if (n0 - 2 >= 0)
+      h2 = load2(u + (n0 - 2) * S, x, y, nx, ny, hl ? hl + (long long)(n0 - 2) * nx : nullptr,
+                 hr ? hr + (long long)(n0 - 2) * nx : nullptr);
   }
   const int n1 = min(n0 + kTC, p.nt);
 #pragma unroll 4
   for (int n = n0; n < n1; ++n) {
     N2 h0 = {0, 0, 0, 0, 0};
-    if (act) h0 = load2(u + n * S, x, y, nx, ny);
+    if (act)
+      h0 = load2(u + n * S, x, y, nx, ny, hl ? hl + (long long)n * nx : nullptr, hr ? hr + (long long)n * nx : nullptr);
     const double yc = tp.c2[0] * h0.c + tp.c2[1] * h1.c + tp.c2[2] * h2.c;
     const double yxm = tp.c2[0] * h0.xm + tp.c2[1] * h1.xm + tp.c2[2] * h2.xm;
     const double yxp = tp.c2[0] * h0.xp + tp.c2[1] * h1.xp + tp.c2[2] * h2.xp;
@@ -154,12 +164,15 @@ __global__ void __launch_bounds__(kBX) stencil2d_kernel(pd_stencil p, const doub
 
 // ---------------- right-hand side ----------------
 // K v at spatial point s of a single time level (zero Dirichlet / periodic wrap)
-PD_D double applyK(const pd_stencil& p, const double* __restrict__ v, long long s) {
+PD_D double applyK(const pd_stencil& p, const double* __restrict__ v, long long s, int which) {
+  const int hw = p.op == 2 ? p.nx : 1;
+  const double* hl = p.hlo ? p.hlo + which * hw : nullptr;
+  const double* hr = p.hhi ? p.hhi + which * hw : nullptr;
   if (p.op == 2) {
-    const N2 h = load2(v, (int)(s % p.nx), (int)(s / p.nx), p.nx, p.ny);
+    const N2 h = load2(v, (int)(s % p.nx), (int)(s / p.nx), p.nx, p.ny, hl, hr);
     return p.k2c * h.c + p.k2x_m * h.xm + p.k2x_p * h.xp + p.k2y_m * h.ym + p.k2y_p * h.yp;
   }
-  const N1 h = load1(v, (int)s, p.nx);
+  const N1 h = load1(v, (int)s, p.nx, hl, hr);
   return p.sub * h.l + p.dia * h.c + p.sup * h.r;
 }
 
@@ -177,14 +190,14 @@ __global__ void rhs_kernel(pd_stencil p, const double* __restrict__ u0, const do
       if (f) v = (n == 0) ? 0.5 * f[s] : f[(long long)n * S + s];
       if (n == 0) {
         v += u0[s] * i2;
-        if (v0) v += v0[s] / p.dt + 0.5 * p.dt * applyK(p, v0, s);
+        if (v0) v += v0[s] / p.dt + 0.5 * p.dt * applyK(p, v0, s, 1);
       } else if (n == 1) {
-        v += -u0[s] * i2 - 0.5 * applyK(p, u0, s);
+        v += -u0[s] * i2 - 0.5 * applyK(p, u0, s, 0);
       }
     } else {
       // theta-method (P:l.321-323, reading c5): b_n = theta f_n + (1-theta) f_{n-1}; b_1 += (I/dt - (1-theta)K) U0
       if (f) v = p.theta * f[(long long)(n + 1) * S + s] + (1.0 - p.theta) * f[(long long)n * S + s];
-      if (n == 0) v += u0[s] / p.dt - (1.0 - p.theta) * applyK(p, u0, s);
+      if (n == 0) v += u0[s] / p.dt - (1.0 - p.theta) * applyK(p, u0, s, 0);
     }
     b[i] = v;
   }
