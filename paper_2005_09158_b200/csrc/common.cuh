@@ -33,4 +33,9 @@ PD_HD double2 crcp(double2 a) {
   return make_double2(ax * d, -ay * d);
 }
 PD_HD double2 cdiv(double2 a, double2 b) { return cmul(a, crcp(b)); }
+// 1/a with one correctly rounded fp64 reciprocal (no overflow guard: for |a| in ~[1e-150, 1e150])
+PD_D double2 crcp_fast(double2 a) {
+  const double d = __drcp_rn(fma(a.x, a.x, a.y * a.y));
+  return make_double2(a.x * d, -a.y * d);
+}
 PD_HD double2 czero() { return make_double2(0.0, 0.0); }

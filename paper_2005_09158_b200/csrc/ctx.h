@@ -92,6 +92,17 @@ struct pd_ctx {
   // host-buffer staging
   double* stage_a = nullptr;
   double* stage_b = nullptr;
+  // CUDA graphs of the apply, keyed by (r, z, accumulate) (PD_GRAPH=1)
+  struct GraphEntry {
+    const double* r;
+    double* z;
+    int acc;
+    cudaGraphExec_t exec;
+    long long launches;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = false;
+  cudaStream_t cap_stream = nullptr;  // private stream for capture (the legacy stream cannot capture)
   // diagnostics
   long long launches = 0;
   bool timing = false;

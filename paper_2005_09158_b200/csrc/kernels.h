@@ -69,6 +69,7 @@ struct pd_stencil {
   // rhs: [2][hw] = neighbour values of U_0 (row 0) and V_0 (row 1).
   const double* hlo;
   const double* hhi;
+  double c1[3], c2[3];  // time taps (filled by pd_launch_stencil from scheme, dt, theta)
 };
 // out = b - A u (b != NULL) or out = A u (b == NULL); per-block partial sums of out^2 into partial[]
 cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double* u, double* out, double* partial,

@@ -129,6 +129,8 @@ static void free_ctx(pd_ctx* c) {
     if (p) cudaFree(p);
   for (double* p : c->V) cudaFree(p);
   if (c->hred) cudaFreeHost(c->hred);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   pd_dist_free(c);
   for (auto& e : c->evpool)
     if (e) cudaEventDestroy(e);
@@ -333,6 +335,7 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
 
   // ---- four-step time FFT for long time axes ----
   c->use_tf4 = pd_tf4_supported(nt) && getenv("PD_NO_TF4") == nullptr;
+  c->use_graphs = getenv("PD_GRAPH") != nullptr && atoi(getenv("PD_GRAPH")) != 0;
   if (c->use_tf4) {
     const int n2 = pd_tf4_n2(), n1 = nt / n2, ppt = pd_tf4_pairs_per_tile();
     std::vector<double2> h1 = twiddles(n1), h2 = twiddles(n2);
@@ -514,14 +517,47 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
   return PD_OK;
 }
 
-// z = P^{-1} r, or u += P^{-1} r when accumulate
-static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
+static pd_status apply_direct(pd_ctx* c, const double* r, double* z, int accumulate) {
   if (c->dist_mode != 0) return pd_dist_apply(c, r, z, accumulate);
   pd_status s = pd_time_fft_fwd(c, r, c->Sh, c->S);
   if (s != PD_OK) return s;
   s = pd_spatial_solve(c, c->Sh, c->F, 0);
   if (s != PD_OK) return s;
   return pd_time_fft_inv(c, c->Sh, z, c->S, accumulate);
+}
+
+// z = P^{-1} r, or u += P^{-1} r when accumulate.  With graphs enabled (single GPU, phase timing off) the
+// launch sequence of each (r, z, accumulate) triple is captured once and replayed as one CUDA graph.
+static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
+  if (!c->use_graphs || c->dist_mode != 0 || c->timing) return apply_direct(c, r, z, accumulate);
+  for (auto& g : c->graphs)
+    if (g.r == r && g.z == z && g.acc == accumulate) {
+      PD_CUDA(c, cudaGraphLaunch(g.exec, c->st));
+      c->launches += g.launches;
+      return PD_OK;
+    }
+  if (c->graphs.size() >= 64) {
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  const long long l0 = c->launches;
+  if (!c->cap_stream) PD_CUDA(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t user = c->st;
+  c->st = c->cap_stream;
+  PD_CUDA(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+  pd_status s = apply_direct(c, r, z, accumulate);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+  c->st = user;
+  if (s != PD_OK) return s;
+  if (e != cudaSuccess) return fail(c, PD_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(c, PD_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  c->graphs.push_back({r, z, accumulate, exec, c->launches - l0});
+  PD_CUDA(c, cudaGraphLaunch(exec, c->st));
+  return PD_OK;
 }
 
 // out = b - A u (b != NULL) or A u; if norm2 != NULL: deterministic ||out||^2 into *norm2 (host, syncs)

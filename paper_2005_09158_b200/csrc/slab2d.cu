@@ -92,7 +92,7 @@ slab_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict_
         for (int m = 0; m < RL; ++m) {
           const int ky = j + m * s;
           const double2 kap = make_double2(fma(prm.kd, s_sx[ky], ax), fma(prm.cy, s_sn[ky], bx));
-          sm[soff<s * C>(a, m)] = cscale(cdiv(w[m], cfma(l2, kap, l1)), invNN);
+          sm[soff<s * C>(a, m)] = cscale(cmul(w[m], crcp_fast(cfma(l2, kap, l1))), invNN);
         }
       });
   __syncthreads();

@@ -17,7 +17,7 @@ struct Taps {
   int ntaps;
 };
 
-PD_D Taps taps_of(const pd_stencil& p) {
+PD_HD Taps taps_of(const pd_stencil& p) {
   Taps t;
   if (p.scheme == 2) {
     const double i2 = 1.0 / (p.dt * p.dt);
@@ -44,7 +44,7 @@ PD_D N1 load1(const double* __restrict__ row, int x, int nx, const double* hl, c
   return v;
 }
 
-__global__ void __launch_bounds__(kBX) stencil1d_kernel(pd_stencil p, const double* __restrict__ b,
+__global__ void __launch_bounds__(kBX, 4) stencil1d_kernel(pd_stencil p, const double* __restrict__ b,
                                                        const double* __restrict__ u, double* __restrict__ out,
                                                        double* __restrict__ partial) {
   const Taps tp = taps_of(p);
@@ -107,58 +107,123 @@ PD_D N2 load2(const double* __restrict__ slab, int x, int y, int nx, int ny, con
   return v;
 }
 
-__global__ void __launch_bounds__(kBX) stencil2d_kernel(pd_stencil p, const double* __restrict__ b,
-                                                       const double* __restrict__ u, double* __restrict__ out,
-                                                       double* __restrict__ partial) {
-  const Taps tp = taps_of(p);
+// Tile of 32 x-points (one warp) by kTY y-rows per block plus two halo warps (rows y0-1 and ylast+1), walking
+// kTC time rows.  Each lane loads only its own point per row (one coalesced load); the time combination
+// y = sum_k c2_k u_{n-k} of the x-neighbours arrives by warp shuffle (lanes at a tile or domain edge load
+// their outside neighbour themselves) and of the y-neighbours through a double-buffered shared row.
+constexpr int kTY = 16;
+constexpr int kW2 = kTY + 2;
+#ifndef PD_STENCIL2D_MINB
+#define PD_STENCIL2D_MINB 2
+#endif
+
+struct Hist { double h0, h1, h2; };
+
+// NT = number of time taps (2: theta-method, 3: leapfrog); taps read from the parameter bank
+template <int NT>
+PD_D double comb(const pd_stencil& p, const Hist& h) {
+  return NT == 3 ? p.c2[0] * h.h0 + p.c2[1] * h.h1 + p.c2[2] * h.h2 : p.c2[0] * h.h0 + p.c2[1] * h.h1;
+}
+template <int NT>
+PD_D double comb1(const pd_stencil& p, const Hist& h) {
+  return NT == 3 ? p.c1[0] * h.h0 + p.c1[1] * h.h1 + p.c1[2] * h.h2 : p.c1[0] * h.h0 + p.c1[1] * h.h1;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(pd_stencil p, const double* __restrict__ b,
+                                                             const double* __restrict__ u, double* __restrict__ out,
+                                                             double* __restrict__ partial) {
+  __shared__ double ysh[2][kW2][32];
+  __shared__ double red[kW2];
   const int nx = p.nx, ny = p.ny;
   const long long S = (long long)nx * ny;
-  const long long s = (long long)blockIdx.x * kBX + threadIdx.x;
-  const bool act = s < S;
-  const int x = act ? (int)(s % nx) : 0, y = act ? (int)(s / nx) : 0;
-  const int n0 = blockIdx.y * kTC;
-  double acc = 0.0;
-  N2 h1 = {0, 0, 0, 0, 0}, h2 = {0, 0, 0, 0, 0};
-  const double* hl = p.hlo;
-  const double* hr = p.hhi;
-  if (act) {
-    if (n0 - 1 >= 0)
-      h1 = load2(u + (n0 - 1) * S, x, y, nx, ny, hl ? hl + (long long)(n0 - 1) * nx : nullptr,
-                 hr ? hr + (long long)(n0 - 1) * nx : nullptr);
-    if (n0 - 2 >= 0)
-      h2 = load2(u + (n0 - 2) * S, x, y, nx, ny, hl ? hl + (long long)(n0 - 2) * nx : nullptr,
-                 hr ? hr + (long long)(n0 - 2) * nx : nullptr);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * kTY;
+  const int ylast = min(y0 + kTY, ny) - 1;
+  const int xr = x0 + lane;
+  const bool xin = xr < nx;
+  const int x = xin ? xr : nx - 1;
+  // warp 0..kTY-1: output rows y0+warp; warp kTY: row y0-1; warp kTY+1: row ylast+1
+  int srow;  // shared row slot
+  int y;
+  const double* hsrc = nullptr;  // halo rows of a neighbouring rank ([nt][nx]) replacing the wrap
+  if (warp < kTY) {
+    y = y0 + warp;
+    srow = warp + 1;
+  } else if (warp == kTY) {
+    y = y0 - 1;
+    srow = 0;
+    if (y < 0) { y = ny - 1; hsrc = p.hlo; }
+  } else {
+    y = ylast + 1;
+    srow = ylast - y0 + 2;
+    if (y >= ny) { y = 0; hsrc = p.hhi; }
   }
+  const bool outw = warp < kTY && y <= ylast;
+  const bool act = outw && xin;
+  const bool live = warp >= kTY || y <= ylast;  // rows whose combination is needed
+  const bool needL = outw && (lane == 0 || x == 0);
+  const bool needR = outw && (lane == 31 || x == nx - 1);
+  const int xl = x == 0 ? nx - 1 : x - 1, xp = x == nx - 1 ? 0 : x + 1;
+  const double* rowp = hsrc ? hsrc : u + (long long)y * nx;
+  const long long rstride = hsrc ? nx : S;  // time stride of this warp's row
+  const int n0 = blockIdx.z * kTC;
   const int n1 = min(n0 + kTC, p.nt);
-#pragma unroll 4
+  // per-row pointers advanced by the time stride (row n0); loads of rows < 0 are skipped
+  const double* pc = rowp + (long long)n0 * rstride + x;
+  const int dl = xl - x, dr = xp - x;
+  auto ld = [&](const double* q, int n, int d) -> double { return (n >= 0 && live) ? q[d] : 0.0; };
+  Hist c = {0.0, ld(pc - rstride, n0 - 1, 0), NT == 3 ? ld(pc - 2 * rstride, n0 - 2, 0) : 0.0};
+  Hist L = {0.0, 0.0, 0.0}, R = {0.0, 0.0, 0.0};
+  if (needL) { L.h1 = ld(pc - rstride, n0 - 1, dl); if (NT == 3) L.h2 = ld(pc - 2 * rstride, n0 - 2, dl); }
+  if (needR) { R.h1 = ld(pc - rstride, n0 - 1, dr); if (NT == 3) R.h2 = ld(pc - 2 * rstride, n0 - 2, dr); }
+  const long long off = (long long)n0 * S + (long long)y * nx + x;
+  const double* pb = b ? b + off : nullptr;
+  double* po = out + off;
+  // one-row prefetch
+  double nc = live ? pc[0] : 0.0, nl = needL ? pc[dl] : 0.0, nr = needR ? pc[dr] : 0.0;
+  double nb = (act && pb) ? pb[0] : 0.0;
+  double acc = 0.0;
+  int buf = 0;
   for (int n = n0; n < n1; ++n) {
-    N2 h0 = {0, 0, 0, 0, 0};
-    if (act)
-      h0 = load2(u + n * S, x, y, nx, ny, hl ? hl + (long long)n * nx : nullptr, hr ? hr + (long long)n * nx : nullptr);
-    const double yc = tp.c2[0] * h0.c + tp.c2[1] * h1.c + tp.c2[2] * h2.c;
-    const double yxm = tp.c2[0] * h0.xm + tp.c2[1] * h1.xm + tp.c2[2] * h2.xm;
-    const double yxp = tp.c2[0] * h0.xp + tp.c2[1] * h1.xp + tp.c2[2] * h2.xp;
-    const double yym = tp.c2[0] * h0.ym + tp.c2[1] * h1.ym + tp.c2[2] * h2.ym;
-    const double yyp = tp.c2[0] * h0.yp + tp.c2[1] * h1.yp + tp.c2[2] * h2.yp;
-    double Au = tp.c1[0] * h0.c + tp.c1[1] * h1.c + tp.c1[2] * h2.c;
-    Au += p.k2c * yc + p.k2x_m * yxm + p.k2x_p * yxp + p.k2y_m * yym + p.k2y_p * yyp;
+    c.h0 = nc; L.h0 = nl; R.h0 = nr;
+    const double bv = nb;
+    if (n + 1 < n1) {
+      pc += rstride;
+      if (live) nc = pc[0];
+      if (needL) nl = pc[dl];
+      if (needR) nr = pc[dr];
+      if (act && pb) nb = pb[S];
+    }
+    const double yc = comb<NT>(p, c);
+    if (live) ysh[buf][srow][lane] = yc;  // rows past ylast share the slot of the high halo row
+    const double up = __shfl_up_sync(0xffffffffu, yc, 1);
+    const double dn = __shfl_down_sync(0xffffffffu, yc, 1);
+    const double yxm = needL ? comb<NT>(p, L) : up;
+    const double yxp = needR ? comb<NT>(p, R) : dn;
+    __syncthreads();
     if (act) {
-      const long long idx = n * S + s;
-      const double v = b ? b[idx] - Au : Au;
-      out[idx] = v;
+      const double yym = ysh[buf][srow - 1][lane], yyp = ysh[buf][srow + 1][lane];
+      double Au = comb1<NT>(p, c);
+      Au += p.k2c * yc + p.k2x_m * yxm + p.k2x_p * yxp + p.k2y_m * yym + p.k2y_p * yyp;
+      const double v = pb ? bv - Au : Au;
+      *po = v;
       acc = fma(v, v, acc);
     }
-    h2 = h1;
-    h1 = h0;
+    po += S;
+    if (pb) pb += S;
+    c.h2 = c.h1; c.h1 = c.h0;
+    L.h2 = L.h1; L.h1 = L.h0;
+    R.h2 = R.h1; R.h1 = R.h0;
+    buf ^= 1;
   }
-  __shared__ double red[kBX / 32];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  if (lane == 0) red[warp] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < kBX / 32; ++w) t += red[w];
-    partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    for (int w = 0; w < kTY; ++w) t += red[w];
+    partial[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
   }
 }
 
@@ -203,24 +268,35 @@ __global__ void rhs_kernel(pd_stencil p, const double* __restrict__ u0, const do
   }
 }
 
+Taps taps_host(const pd_stencil& p) { return taps_of(p); }
+
 }  // namespace
+
+int pd_stencil_num_blocks(const pd_stencil& p) {
+  const long long nz = (p.nt + kTC - 1) / kTC;
+  if (p.op == 2) return (int)(((p.nx + 31) / 32) * ((p.ny + kTY - 1) / kTY) * nz);
+  return (int)(((p.nx + kBX - 1) / kBX) * nz);
+}
 
 cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double* u, double* out, double* partial,
                               int* nblocks_out, cudaStream_t st) {
-  const long long S = (long long)p.nx * p.ny;
-  dim3 grid((unsigned)((S + kBX - 1) / kBX), (unsigned)((p.nt + kTC - 1) / kTC));
-  if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
-  if (p.op == 2)
-    stencil2d_kernel<<<grid, kBX, 0, st>>>(p, b, u, out, partial);
-  else
+  if (nblocks_out) *nblocks_out = pd_stencil_num_blocks(p);
+  if (p.op == 2) {
+    dim3 grid((unsigned)((p.nx + 31) / 32), (unsigned)((p.ny + kTY - 1) / kTY), (unsigned)((p.nt + kTC - 1) / kTC));
+    pd_stencil q = p;
+    const Taps t = taps_host(p);
+    for (int k = 0; k < 3; ++k) { q.c1[k] = t.c1[k]; q.c2[k] = t.c2[k]; }
+    if (t.ntaps == 3)
+      stencil2d_kernel<3><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
+    else
+      stencil2d_kernel<2><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
+  } else {
+    dim3 grid((unsigned)((p.nx + kBX - 1) / kBX), (unsigned)((p.nt + kTC - 1) / kTC));
     stencil1d_kernel<<<grid, kBX, 0, st>>>(p, b, u, out, partial);
+  }
   return cudaGetLastError();
 }
 
-int pd_stencil_num_blocks(const pd_stencil& p) {
-  const long long S = (long long)p.nx * p.ny;
-  return (int)(((S + kBX - 1) / kBX) * ((p.nt + kTC - 1) / kTC));
-}
 
 cudaError_t pd_launch_rhs(const pd_stencil& p, const double* u0, const double* v0, const double* f, double* b,
                           cudaStream_t st) {

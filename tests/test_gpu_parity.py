@@ -124,7 +124,8 @@ def test_apply_cfg4_full_properties():
 # ------------------------------------------------------------------------------------------------ residual / rhs
 @pytest.mark.parametrize("op,scheme,nx,nt", [(W.ADE1D, W.BE, 63, 32), (W.ADE1D, W.CN, 1000, 70),
                                              (W.WAVE1D, W.LF, 333, 40), (W.ADE2D, W.BE, 64, 33),
-                                             (W.ADE2D, W.CN, 32, 100)])
+                                             (W.ADE2D, W.CN, 32, 100), (W.ADE2D, W.CN, 16, 37),
+                                             (W.ADE2D, W.BE, 128, 130), (W.ADE2D, W.CN, 1024, 4)])
 def test_residual_matvec_rhs_match_oracle(op, scheme, nx, nt):
     nt_pow2 = 1 << (nt - 1).bit_length()
     cfg = _cfg(op, scheme, nx, nt_pow2)
