@@ -8,10 +8,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparadiag.so")
-SOURCES = ["paradiag.cpp", "dist.cpp", "comm.cpp", "tfft.cu", "tfft4.cu", "tridiag.cu", "slab2d.cu", "stencil.cu", "blas1.cu"]
+SOURCES = ["paradiag.cpp", "dist.cpp", "comm.cpp", "tfft.cu", "tfft4.cu", "tfx.cu", "tridiag.cu", "slab2d.cu", "stencil.cu", "blas1.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
+# tuning experiments only (tools/): extra -D flags and an alternative output path
+FLAGS += os.environ.get("PD_NVCC_EXTRA", "").split()
+LIB = os.environ.get("PD_LIB_OUT", LIB)
 
 
 def _stale() -> bool:
@@ -25,7 +28,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if LIB.endswith("paper_2005_09158_b200/libparadiag.so") else "build_var")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -67,6 +67,7 @@ struct pd_ctx {
   double2* tf4_scratch = nullptr;
   long long tf4_chunk = 0;
   bool use_tf4 = false;
+  bool use_tfx = false;           // 2D: four-step time FFT with the x-FFT folded in (tfx.cu)
   double2* lam1 = nullptr;       // half spectrum, F entries
   double2* lam2 = nullptr;
   pd_tri_coef* tri = nullptr;    // 1D

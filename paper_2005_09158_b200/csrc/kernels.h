@@ -42,6 +42,20 @@ cudaError_t pd_launch_tridiag(double2* Sh, int nx, int nfreq, const pd_tri_coef*
 int pd_tridiag_rows_per_thread();
 int pd_tridiag_threads(int nx);
 
+// ---- Steps (a)/(c), 2D periodic, with the x-FFT of Step (b) folded in (tfx.cu): N1 = 8, N2 = Nt/8 ----
+// The spectrum then holds X_n[y][kx]; Step (b) runs only the slab column pass (pd_launch_slab2d cols_only).
+// chunk_pairs must be a multiple of pd_tfx_chunk_align (whole x-rows); tables: tw2 = N2-point, twt = Nt-point,
+// twx = NX-point twiddles.
+int pd_tfx_supported(int nt, int nx);
+int pd_tfx_n2(int nt);
+long long pd_tfx_chunk_align(int nt, int nx);
+cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
+                              const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
+                              cudaStream_t st, int* nl);
+cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
+                              const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
+                              int accumulate, cudaStream_t st, int* nl);
+
 // ---- Step (b), 2D periodic: per-frequency slab 2D FFT -> divide -> inverse 2D FFT (slab2d.cu) ----
 // denominators lambda1_n + lambda2_n kappa(kx, ky), kappa = kd*(sx[kx]+sx[ky]) + i*(ax sn[kx] + ay sn[ky])/h
 struct pd_slab_params {
@@ -53,7 +67,7 @@ int pd_slab2d_chunk(int n, int nfreq);
 // chunk = slabs per L2-resident chunk; *launches = kernels launched
 cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                              const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
-                             int chunk, cudaStream_t st, int* launches);
+                             int chunk, int cols_only, cudaStream_t st, int* launches);
 
 // ---- all-at-once residual / matvec (stencil.cu) ----
 struct pd_stencil {

@@ -333,23 +333,26 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     }
   }
 
-  // ---- four-step time FFT for long time axes ----
-  c->use_tf4 = pd_tf4_supported(nt) && getenv("PD_NO_TF4") == nullptr;
+  // ---- four-step time FFT for long time axes (1D), or with the x-FFT folded in (2D, tfx.cu) ----
+  c->use_tfx = g->op == PD_ADE2D_PERIODIC && pd_tfx_supported(nt, g->nx) && getenv("PD_NO_TFX") == nullptr;
+  c->use_tf4 = !c->use_tfx && pd_tf4_supported(nt) && getenv("PD_NO_TF4") == nullptr;
   c->use_graphs = getenv("PD_GRAPH") != nullptr && atoi(getenv("PD_GRAPH")) != 0;
-  if (c->use_tf4) {
-    const int n2 = pd_tf4_n2(), n1 = nt / n2, ppt = pd_tf4_pairs_per_tile();
+  if (c->use_tf4 || c->use_tfx) {
+    const int n2 = c->use_tfx ? pd_tfx_n2(nt) : pd_tf4_n2(), n1 = nt / n2;
+    const long long align = c->use_tfx ? pd_tfx_chunk_align(nt, g->nx) : pd_tf4_pairs_per_tile();
     std::vector<double2> h1 = twiddles(n1), h2 = twiddles(n2);
     SETUP_CUDA(dalloc(&c->tw_n1, n1));
     SETUP_CUDA(dalloc(&c->tw_n2, n2));
     SETUP_CUDA(cudaMemcpy(c->tw_n1, h1.data(), n1 * sizeof(double2), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->tw_n2, h2.data(), n2 * sizeof(double2), cudaMemcpyHostToDevice));
     const long long npairs = (c->S + 1) / 2;
-    // column chunk of the stage-1 -> stage-2 scratch (default 1 GB: launch count beats L2 residency, §5)
+    // column chunk of the stage-1 -> stage-2 scratch (default 1 GB: launch count beats L2 residency, §5);
+    // 2D: whole x-rows
     const char* mb_env = getenv("PD_TF4_CHUNK_MB");
     const long long mb = mb_env ? atoll(mb_env) : 1024;
-    long long chunk = ((mb << 20) / ((long long)nt * 16)) / ppt * ppt;
-    if (chunk < ppt) chunk = ppt;
-    if (chunk > npairs) chunk = (npairs + ppt - 1) / ppt * ppt;
+    long long chunk = ((mb << 20) / ((long long)nt * 16)) / align * align;
+    if (chunk < align) chunk = align;
+    if (chunk > npairs) chunk = (npairs + align - 1) / align * align;
     c->tf4_chunk = chunk;
     SETUP_CUDA(dalloc(&c->tf4_scratch, (size_t)nt * chunk));
   }
@@ -477,7 +480,7 @@ pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   if (c->g.op == PD_ADE2D_PERIODIC) {
     int nl = 0;
     PD_CUDA(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
-                                c->slab_chunk, c->st, &nl));
+                                c->slab_chunk, c->use_tfx ? 1 : 0, c->st, &nl));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tridiag(Sh, c->g.nx, nfreq, c->tri + f0, pd_tridiag_rows_per_thread(), c->st));
@@ -490,7 +493,11 @@ pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
 pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) {
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   phase_begin(c, 0);
-  if (c->use_tf4) {
+  if (c->use_tfx) {
+    int nl = 0;
+    PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, Sh, S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
+    c->launches += nl;
+  } else if (c->use_tf4) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, Sh, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
     c->launches += nl;
@@ -506,7 +513,12 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   const int ph = accumulate ? 4 : 2;
   phase_begin(c, ph);
-  if (c->use_tf4) {
+  if (c->use_tfx) {
+    int nl = 0;
+    PD_CUDA(c, pd_launch_tfx_inv(c->nt, c->g.nx, Sh, z, S, c->igam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
+                                 accumulate, c->st, &nl));
+    c->launches += nl;
+  } else if (c->use_tf4) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl));
     c->launches += nl;

@@ -4,12 +4,11 @@
 //   kappa(kx, ky) = (4 nu/h^2)(sin^2(pi kx/N) + sin^2(pi ky/N)) + i (ax sin(2 pi kx/N) + ay sin(2 pi ky/N))/h
 // (reading c14), so each slab is solved exactly by   2D FFT -> divide by lambda1 + lambda2 kappa -> 2D IFFT.
 //
-// The half-spectrum buffer holds F slabs of N x N complex.  Slabs are processed in chunks small enough to
-// stay L2-resident (<= ~48 MB); per chunk three launches run in place: (1) row FFTs along x (rows are
-// contiguous), (2) column FFT along y + divide + column IFFT (8 adjacent columns per CTA = 128 B row
-// segments), (3) row IFFTs along x.  Every launch has full occupancy (thousands of CTAs); HBM sees the
-// chunk once on the way in (launch 1 reads) and once on the way out (write-back of launch 3), the two
-// transposes go through L2 (~12.5 TB/s r+w measured on this B200 pool).
+// The half-spectrum buffer holds F slabs of N x N complex, processed in chunks of slabs (~1 GB: launch
+// count, not L2 residency, decides on B200); per chunk three launches run in place:
+// (1) row FFTs along x (rows are contiguous), (2) column FFT along y + divide + column IFFT (8 adjacent
+// columns per CTA = 128 B row segments), (3) row IFFTs along x.  When the time FFTs already did the x
+// transforms (tfx.cu, the default where supported) only launch (2) runs (cols_only).
 #include "fft.cuh"
 #include "kernels.h"
 
@@ -24,7 +23,23 @@ struct SlabCfg {
   static constexpr int C = kBatch;
   static constexpr int E = elems_per_thread(N);
   static constexpr int NTH = C * N / E;
-  static constexpr int MINB = NTH <= 256 ? 2 : 1;
+#ifndef PD_SLAB_MINB
+#define PD_SLAB_MINB 3
+#endif
+  static constexpr int MINB = NTH <= 256 ? PD_SLAB_MINB : 1;
+};
+
+// column kernel: radix cap RM (8 halves the register footprint and doubles the threads per tile)
+#ifndef PD_SLAB_COLS_RM
+#define PD_SLAB_COLS_RM 8
+#endif
+template <int N>
+struct ColCfg {
+  static constexpr int C = kBatch;
+  static constexpr int RM = PD_SLAB_COLS_RM;
+  static constexpr int E = elems_per_thread(N, RM);
+  static constexpr int NTH = C * N / E;
+  static constexpr int MINB = NTH <= 256 ? 2 : NTH <= 512 ? 2 : 1;
 };
 
 // rows [blockIdx.x*C, +C) of the flattened chunk (row index over slabs: slab*N + y), FFT along x in place
@@ -54,28 +69,23 @@ slab_rows_kernel(double2* __restrict__ base, const double2* __restrict__ tw) {
 
 // columns [c0, c0 + C) of slab (slab0 + blockIdx.y): forward FFT along y, divide, inverse FFT along y
 template <int N>
-__global__ void __launch_bounds__(SlabCfg<N>::NTH, SlabCfg<N>::MINB)
+__global__ void __launch_bounds__(ColCfg<N>::NTH, ColCfg<N>::MINB)
 slab_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict__ lam1,
                  const double2* __restrict__ lam2, const double* __restrict__ sx, const double* __restrict__ sn,
                  pd_slab_params prm, const double2* __restrict__ tw) {
-  using T = SlabCfg<N>;
-  constexpr int C = T::C, NTH = T::NTH, R0 = first_radix(N), RL = last_radix(N);
+  using T = ColCfg<N>;
+  constexpr int C = T::C, NTH = T::NTH, RM = T::RM, R0 = first_radix(N, RM), RL = last_radix(N, RM);
   extern __shared__ double2 sm[];
   __shared__ double2 s_tw[N];
-  __shared__ double s_sx[N], s_sn[N];
   const int n = slab0 + blockIdx.y;
   const int c0 = blockIdx.x * C;
   double2* slab = Sh + (long long)n * N * N + c0;
   const double2 l1 = lam1[n], l2 = lam2[n];
   const double invNN = 1.0 / ((double)N * (double)N);
   load_table(s_tw, tw, N);
-  for (int i = threadIdx.x; i < N; i += NTH) {
-    s_sx[i] = __ldg(sx + i);
-    s_sn[i] = __ldg(sn + i);
-  }
   __syncthreads();
   // forward FFT along y; the last pass divides by lambda1 + lambda2 kappa(kx, ky) on its way to smem
-  fft_io<N, C, false, false, NTH, false, true>(
+  fft_io<N, C, false, false, NTH, false, true, RM>(
       sm, s_tw,
       [&](int j, auto st, int c, double2* v) {
         constexpr int s = decltype(st)::value;
@@ -86,17 +96,17 @@ slab_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict_
       [&](int j, auto st, int c, const double2* w) {
         constexpr int s = decltype(st)::value;
         const int kx = c0 + c;
-        const double ax = prm.kd * s_sx[kx], bx = prm.cx * s_sn[kx];
+        const double ax = prm.kd * __ldg(sx + kx), bx = prm.cx * __ldg(sn + kx);
         const int a = lin<N, C, false>(j, c);
 #pragma unroll
         for (int m = 0; m < RL; ++m) {
           const int ky = j + m * s;
-          const double2 kap = make_double2(fma(prm.kd, s_sx[ky], ax), fma(prm.cy, s_sn[ky], bx));
+          const double2 kap = make_double2(fma(prm.kd, __ldg(sx + ky), ax), fma(prm.cy, __ldg(sn + ky), bx));
           sm[soff<s * C>(a, m)] = cscale(cmul(w[m], crcp_fast(cfma(l2, kap, l1))), invNN);
         }
       });
   __syncthreads();
-  fft_io<N, C, true, false, NTH, true, false>(
+  fft_io<N, C, true, false, NTH, true, false, RM>(
       sm, s_tw,
       [&](int j, auto st, int c, double2* v) {
         constexpr int s = decltype(st)::value;
@@ -119,8 +129,8 @@ int smem_bytes() {
 
 template <int N>
 cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2* lam2, const double* sx,
-                     const double* sn, pd_slab_params prm, const double2* tw, int chunk, cudaStream_t st,
-                     int* launches) {
+                     const double* sn, pd_slab_params prm, const double2* tw, int chunk, int cols_only,
+                     cudaStream_t st, int* launches) {
   using T = SlabCfg<N>;
   const int smem = smem_bytes<N>();
   static bool attr = false;
@@ -138,10 +148,10 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
     const int ns = nfreq - s0 < chunk ? nfreq - s0 : chunk;
     double2* base = Sh + (long long)s0 * N * N;
     const unsigned row_ctas = (unsigned)(ns * (N / T::C));
-    slab_rows_kernel<N, false><<<row_ctas, T::NTH, smem, st>>>(base, tw);
-    slab_cols_kernel<N><<<dim3(N / T::C, ns), T::NTH, smem, st>>>(Sh, s0, lam1, lam2, sx, sn, prm, tw);
-    slab_rows_kernel<N, true><<<row_ctas, T::NTH, smem, st>>>(base, tw);
-    nl += 3;
+    if (!cols_only) slab_rows_kernel<N, false><<<row_ctas, T::NTH, smem, st>>>(base, tw);
+    slab_cols_kernel<N><<<dim3(N / T::C, ns), ColCfg<N>::NTH, smem, st>>>(Sh, s0, lam1, lam2, sx, sn, prm, tw);
+    if (!cols_only) slab_rows_kernel<N, true><<<row_ctas, T::NTH, smem, st>>>(base, tw);
+    nl += cols_only ? 1 : 3;
   }
   if (launches) *launches = nl;
   return cudaGetLastError();
@@ -162,11 +172,11 @@ int pd_slab2d_chunk(int n, int nfreq) {
 
 cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                              const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
-                             int chunk, cudaStream_t st, int* launches) {
+                             int chunk, int cols_only, cudaStream_t st, int* launches) {
   switch (n) {
 #define PD_CASE(v) \
   case v:          \
-    return launch_n<v>(Sh, nfreq, lam1, lam2, sx, sn, prm, tw, chunk, st, launches);
+    return launch_n<v>(Sh, nfreq, lam1, lam2, sx, sn, prm, tw, chunk, cols_only, st, launches);
     PD_CASE(16) PD_CASE(32) PD_CASE(64) PD_CASE(128) PD_CASE(256) PD_CASE(512) PD_CASE(1024)
 #undef PD_CASE
     default:

@@ -18,8 +18,10 @@
 
 #include "fft.cuh"
 #include "kernels.h"
+#include "tf4_stages.cuh"
 
 using namespace pdfft;
+using namespace pdfft_tf4;
 
 namespace {
 
@@ -30,66 +32,6 @@ template <int N>
 struct Cfg2 {  // stage FFT of length N over C sequences
   static constexpr int E = elems_per_thread(N);
 };
-
-// ---------------------------------------------------------------------------------------------
-// forward stage 1: for fixed t1 (blockIdx.y): N2-point FFT over t2 of rows t1 + N1 t2 of P pairs,
-// times w_Nt^{t1 n2}; writes Y[t1][n2][pl] (scratch rows of Pc pairs).
-// ---------------------------------------------------------------------------------------------
-template <int NT, bool VEC, int RM = 16>
-__global__ void __launch_bounds__(kP * kN2 / RM) tf4_fwd_s1(const double* __restrict__ r, long long S, long long p_begin,
-                                                           long long npairs_chunk, double2* __restrict__ Y,
-                                                           const double* __restrict__ gam,
-                                                           const double2* __restrict__ tw2,
-                                                           const double2* __restrict__ twt) {
-  constexpr int N1 = NT / kN2, C = kP, NTH = kP * kN2 / RM;
-  extern __shared__ double2 sm[];
-  __shared__ double2 s_tw2[kN2], s_twr[kN2];  // 64-point twiddles; w_Nt^{t1 n2}, n2 < 64
-  __shared__ double s_g[kN2];                 // Gamma of rows t1 + N1 t2
-  const int t1 = blockIdx.y;
-  const long long pl0 = (long long)blockIdx.x * kP;  // pair index within the chunk
-  const long long p0 = p_begin + pl0;                // global pair index
-  const long long Pc = npairs_chunk;
-  for (int i = threadIdx.x; i < kN2; i += NTH) {
-    s_tw2[i] = __ldg(tw2 + i);
-    s_twr[i] = __ldg(twt + t1 * i);
-    s_g[i] = __ldg(gam + t1 + N1 * i);
-  }
-  __syncthreads();
-  const bool fullp = pl0 + kP <= Pc;
-  fft_io<kN2, C, false, false, NTH, false, false, RM>(
-      sm, s_tw2,
-      [&](int j, auto st, int c, double2* v) {
-        constexpr int s = decltype(st)::value, R0 = first_radix(kN2, RM);
-        const long long col = 2 * (p0 + c);
-        const double* q = r + (long long)(t1 + N1 * j) * S + col;
-        const long long step = (long long)N1 * s * S;
-        const bool ok = fullp || pl0 + c < Pc;
-        const bool okx = ok && (VEC || col < S), oky = ok && (VEC || col + 1 < S);
-#pragma unroll
-        for (int m = 0; m < R0; ++m) {
-          const double g = s_g[j + m * s];
-          double x = 0.0, y = 0.0;
-          if (VEC) {
-            if (ok) {
-              const double2 u = __ldcs(reinterpret_cast<const double2*>(q + m * step));
-              x = u.x;
-              y = u.y;
-            }
-          } else {
-            if (okx) x = __ldcs(q + m * step);
-            if (oky) y = __ldcs(q + m * step + 1);
-          }
-          v[m] = make_double2(g * x, g * y);
-        }
-      },
-      [&](int j, auto st, int c, const double2* w) {
-        constexpr int s = decltype(st)::value, RL = last_radix(kN2, RM);
-        if (!(fullp || pl0 + c < Pc)) return;
-        double2* q = Y + ((long long)t1 * kN2 + j) * Pc + pl0 + c;
-#pragma unroll
-        for (int m = 0; m < RL; ++m) __stcg(q + (long long)m * s * Pc, cmul(w[m], s_twr[j + m * s]));
-      });
-}
 
 // ---------------------------------------------------------------------------------------------
 // forward stage 2: for the pair of residues (n2, N2-n2) (blockIdx.y = n2 in [0, N2/2]): N1-point FFTs over
@@ -220,69 +162,6 @@ tf4_inv_s1(const double2* __restrict__ Sh, long long S, long long p_begin, long 
       });
 }
 
-// ---------------------------------------------------------------------------------------------
-// inverse stage 2: for fixed t1 (blockIdx.y): N2-point inverse FFT over n2 of W[n2][t1][.], outputs
-// t = t1 + N1 t2 scaled by Gamma^{-1}_t / Nt into the two real columns of each pair (MODE 1: +=).
-// ---------------------------------------------------------------------------------------------
-template <int NT, bool VEC, int MODE, int RM = 16>
-__global__ void __launch_bounds__(kP * kN2 / RM) tf4_inv_s2(const double2* __restrict__ W, long long S, long long p_begin,
-                                                           long long npairs_chunk, double* __restrict__ z,
-                                                           const double* __restrict__ igam,
-                                                           const double2* __restrict__ tw2) {
-  constexpr int N1 = NT / kN2, C = kP, NTH = kP * kN2 / RM;
-  extern __shared__ double2 sm[];
-  __shared__ double2 s_tw2[kN2];
-  __shared__ double s_g[kN2];  // Gamma^{-1} / Nt of rows t1 + N1 t2
-  const int t1 = blockIdx.y;
-  const long long pl0 = (long long)blockIdx.x * kP;
-  const long long p0 = p_begin + pl0;
-  const long long Pc = npairs_chunk;
-  for (int i = threadIdx.x; i < kN2; i += NTH) {
-    s_tw2[i] = __ldg(tw2 + i);
-    s_g[i] = __ldg(igam + t1 + N1 * i) * (1.0 / NT);
-  }
-  __syncthreads();
-  const bool fullp = pl0 + kP <= Pc;
-  fft_io<kN2, C, true, false, NTH, false, false, RM>(
-      sm, s_tw2,
-      [&](int j, auto st, int c, double2* v) {
-        constexpr int s = decltype(st)::value, R0 = first_radix(kN2, RM);
-        const bool ok = fullp || pl0 + c < Pc;
-        const double2* q = W + ((long long)j * N1 + t1) * Pc + pl0 + c;
-#pragma unroll
-        for (int m = 0; m < R0; ++m) v[m] = ok ? __ldcg(q + (long long)m * s * N1 * Pc) : czero();
-      },
-      [&](int j, auto st, int c, const double2* w) {
-        constexpr int s = decltype(st)::value, RL = last_radix(kN2, RM);
-        if (!(fullp || pl0 + c < Pc)) return;
-        const long long col = 2 * (p0 + c);
-        double* q = z + (long long)(t1 + N1 * j) * S + col;
-        const long long step = (long long)N1 * s * S;
-        const bool okx = VEC || col < S, oky = VEC || col + 1 < S;
-#pragma unroll
-        for (int m = 0; m < RL; ++m) {
-          const double g = s_g[j + m * s];
-          double* row = q + m * step;
-          if (VEC) {
-            double2* rp = reinterpret_cast<double2*>(row);
-            if (MODE) {
-              const double2 o = *rp;
-              *rp = make_double2(fma(g, w[m].x, o.x), fma(g, w[m].y, o.y));
-            } else {
-              __stcs(rp, make_double2(g * w[m].x, g * w[m].y));
-            }
-          } else {
-            if (okx) row[0] = MODE ? fma(g, w[m].x, row[0]) : g * w[m].x;
-            if (oky) row[1] = MODE ? fma(g, w[m].y, row[1]) : g * w[m].y;
-          }
-        }
-      });
-}
-
-template <int N>
-int smem_of(int C) {
-  return smem_elems(N * C) * (int)sizeof(double2);
-}
 
 // non-persistent grid versions: one CTA per tile
 template <int NT, int RM>
@@ -292,17 +171,17 @@ void fwd_grid(const double* r, double2* Sh, long long S, const double* gam, cons
   const int sm1 = smem_of<kN2>(kP), sm2 = smem_of<N1>(2 * kP);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tf4_fwd_s1<NT, true, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
-    cudaFuncSetAttribute(tf4_fwd_s1<NT, false, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_fwd_s1<NT, kN2, kP, true, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_fwd_s1<NT, kN2, kP, false, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(tf4_fwd_s2<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     attr = true;
   }
   const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
   const dim3 g1(nt1, N1), g2(nt1, kN2 / 2 + 1);
   if (vec)
-    tf4_fwd_s1<NT, true, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+    tf4_fwd_s1<NT, kN2, kP, true, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
   else
-    tf4_fwd_s1<NT, false, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+    tf4_fwd_s1<NT, kN2, kP, false, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
   tf4_fwd_s2<NT, RM><<<g2, 2 * kP * N1 / elems_per_thread(N1, RM), sm2, st>>>(scratch, S, p, pc, Sh, tb.tw1);
 }
 
@@ -317,10 +196,10 @@ void inv_grid(const double2* Sh, double* z, long long S, const double* igam, con
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tf4_inv_s1<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
-    cudaFuncSetAttribute(tf4_inv_s2<NT, true, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(tf4_inv_s2<NT, true, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(tf4_inv_s2<NT, false, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(tf4_inv_s2<NT, false, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, true, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, true, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, false, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, false, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     attr = true;
   }
   const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
@@ -329,14 +208,14 @@ void inv_grid(const double2* Sh, double* z, long long S, const double* igam, con
   const int th2 = kP * kN2 / RM;
   if (vec) {
     if (accumulate)
-      tf4_inv_s2<NT, true, 1, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+      tf4_inv_s2<NT, kN2, kP, true, 1, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
     else
-      tf4_inv_s2<NT, true, 0, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+      tf4_inv_s2<NT, kN2, kP, true, 0, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
   } else {
     if (accumulate)
-      tf4_inv_s2<NT, false, 1, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+      tf4_inv_s2<NT, kN2, kP, false, 1, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
     else
-      tf4_inv_s2<NT, false, 0, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+      tf4_inv_s2<NT, kN2, kP, false, 0, RM><<<g2, th2, sm2, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
   }
 }
 

@@ -1,0 +1,310 @@
+// Steps (a)/(c) for the 2D periodic problem with the spatial x-FFT of Step (b) folded in.
+//
+// Step (b) in 2D solves every slab by 2D FFT -> divide -> 2D IFFT (slab2d.cu, reading c14).  The x-FFT
+// of the forward 2D FFT commutes with the time DFT of Step (a), and the x-IFFT with that of Step (c), so
+// they are done inside the time-FFT kernels: the spectrum buffer then holds X_n[y][kx] (x already
+// transformed) and Step (b) is a single column pass (y-FFT, divide, y-IFFT).  That removes two full
+// read+write sweeps of the F x N^2 complex spectrum per apply.
+//
+// Four-step time FFT with N1 = 8, N2 = Nt/8 (index maps as in tfft4.cu, eq 2.12, P:l.813-817):
+//   forward  stage 1 (tf4_stages.cuh): N2-point FFTs over t2, twiddle w_Nt^{t1 n2}      -> Y[t1][n2][pair]
+//   forward  stage 2 (here): per (y-row, residue pair n2 / N2-n2): N1-point FFTs over t1 of the 2 x NX/2
+//            packed pair sequences (pair p = real columns 2p, 2p+1, reading c15), then NX/2-point FFTs
+//            over p of the 16 rows, then the even/odd untangle that yields the x-spectrum directly:
+//              A_n = FFT_p(Z_n),  E_n[k] = (A_n[k] + conj A_{Nt-n}[-k]) / 2  (= FFT_p of column 2p of U_n)
+//              O_n[k] = (A_n[k] - conj A_{Nt-n}[-k]) / 2i                     (= FFT_p of column 2p+1)
+//              X_n[kx] = E_n[kx mod NX/2] + w_NX^kx O_n[kx mod NX/2]           for n <= Nt/2
+//   inverse  stage 1 (here): the same maps backwards (E = X[k] + X[k+NX/2], O = (X[k] - X[k+NX/2]) w^-k,
+//            A = E + iO; the mirror rows n > Nt/2 from Hermitian symmetry in time), NX/2-point IFFTs over
+//            p, N1-point IFFTs over n1, twiddle w_Nt^{-t1 n2}                  -> W[n2][t1][pair]
+//   inverse  stage 2 (tf4_stages.cuh): N2-point IFFTs over n2, Gamma^{-1}/Nt, real columns out.
+// A stage-2 / inverse stage-1 tile is one full x-row (NX/2 pairs) x 16 rows of length NX/2: 8 NX complex.
+// All transforms are unnormalised (the slab column pass scales by 1/N^2, as before).
+#include "kernels.h"
+#include "tf4_stages.cuh"
+
+using namespace pdfft;
+using namespace pdfft_tf4;
+
+namespace {
+
+constexpr int kN1 = 8;
+constexpr int kRM = 8;  // the N1 = 8 point DFTs: one radix-8 pass
+#ifndef PD_TFX_RM
+#define PD_TFX_RM 16    // radix cap of the NX/2-point x-direction FFTs (8: NTH = NX, 16: NTH = NX/2)
+#endif
+#ifndef PD_TFX_S1_RM
+#define PD_TFX_S1_RM 16 // radix cap of the N2-point stage FFTs (tf4_stages.cuh)
+#endif
+constexpr int kRX = PD_TFX_RM;
+constexpr int kRS = PD_TFX_S1_RM;
+
+template <int NT, int NX>
+struct Fx {
+  static constexpr int N1 = kN1, N2 = NT / kN1, NP = NX / 2, C = 2 * NP, NTH = 8 * NX / kRX;
+  static constexpr int ROWS = 2 * N1;                 // rows (n1, set) of NP values
+  static constexpr int SMEM = smem_elems(ROWS * NP);  // complex elements
+  static constexpr int KP = 4096 / N2 < 8 ? 8 : 4096 / N2;  // stage-1 pairs per tile (N2 * KP = 4096)
+};
+
+// ---------------------------------------------------------------------------------------------
+// forward stage 2 + x-FFT
+// ---------------------------------------------------------------------------------------------
+template <int NT, int NX>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_fwd_s2(const double2* __restrict__ Y, long long S,
+                                                             long long p_begin, long long Pc,
+                                                             double2* __restrict__ Sh,
+                                                             const double2* __restrict__ twx) {
+  using F = Fx<NT, NX>;
+  constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, C = F::C, NTH = F::NTH;
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_twx[NX], s_twp[NP];
+  const int n2 = blockIdx.y, n2p = (N2 - n2) % N2;
+  const long long pl0 = (long long)blockIdx.x * NP;  // first pair of this x-row within the chunk
+  const long long p0 = p_begin + pl0;
+  for (int i = threadIdx.x; i < NX; i += NTH) {
+    const double2 w = __ldg(twx + i);
+    s_twx[i] = w;
+    if (!(i & 1)) s_twp[i >> 1] = w;
+  }
+  // (1) N1-point DFTs over t1 of the sequences c = (set, p); row (n1, set) keeps p contiguous
+  fft_io<N1, C, false, false, NTH, false, true, kRM>(
+      sm, s_twp,
+      [&](int, auto, int c, double2* v) {
+        const int rr = c < NP ? n2 : n2p, pc = c & (NP - 1);
+        const double2* q = Y + (long long)rr * Pc + pl0 + pc;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = __ldcg(q + (long long)m * N2 * Pc);
+      },
+      [&](int, auto, int c, const double2* w) {
+        const int set = c < NP ? 0 : 1, pc = c & (NP - 1);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) sm[pad((2 * m + set) * NP + pc)] = w[m];
+      });
+  __syncthreads();
+  // (2) NP-point FFTs over p of the 16 rows, in place
+  fft_io<NP, 2 * N1, false, true, NTH, true, true, kRX>(
+      sm, s_twp,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(NP, kRX);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = sm[pad(c * NP + j + m * s)];
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(NP, kRX);
+#pragma unroll
+        for (int m = 0; m < RL; ++m) sm[pad(c * NP + j + m * s)] = w[m];
+      });
+  __syncthreads();
+  // (3) untangle the two real columns of each pair and combine the even/odd halves into X_n[kx]
+  const int nsets = n2p == n2 ? 1 : 2;
+  const int total = nsets * N1 * NX;
+  for (int o = threadIdx.x; o < total; o += NTH) {
+    const int kx = o & (NX - 1);
+    const int rowi = o / NX, set = rowi / N1, n1 = rowi % N1;
+    const int n = (set ? n2p : n2) + N2 * n1;
+    if (n > NT / 2) continue;
+    const int m = (NT - n) & (NT - 1);
+    const int setp = (m % N2) == n2 ? 0 : 1, n1p = m / N2;
+    const int k = kx & (NP - 1);
+    const double2 a = sm[pad((2 * n1 + set) * NP + k)];
+    const double2 b = sm[pad((2 * n1p + setp) * NP + ((NP - k) & (NP - 1)))];
+    const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));     // (a + conj b) / 2
+    const double2 O = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));    // (a - conj b) / 2i
+    __stcs(Sh + (long long)n * S + 2 * p0 + kx, cfma(s_twx[kx], O, E));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// x-IFFT + inverse stage 1
+// ---------------------------------------------------------------------------------------------
+template <int NT, int NX>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_inv_s1(const double2* __restrict__ Sh, long long S,
+                                                             long long p_begin, long long Pc,
+                                                             double2* __restrict__ W,
+                                                             const double2* __restrict__ twx,
+                                                             const double2* __restrict__ twt) {
+  using F = Fx<NT, NX>;
+  constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, C = F::C, NTH = F::NTH;
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_twx[NX], s_twp[NP], s_twa[N1], s_twb[N1];
+  const int n2 = blockIdx.y, n2p = (N2 - n2) % N2;
+  const long long pl0 = (long long)blockIdx.x * NP;
+  const long long p0 = p_begin + pl0;
+  for (int i = threadIdx.x; i < NX; i += NTH) {
+    const double2 w = __ldg(twx + i);
+    s_twx[i] = w;
+    if (!(i & 1)) s_twp[i >> 1] = w;
+  }
+  if (threadIdx.x < N1) {
+    s_twa[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2));
+    s_twb[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2p));
+  }
+  __syncthreads();
+  // (0) rows n <= Nt/2 of the residue set -> A_n = E_n + i O_n and the mirror row A_{Nt-n}[-k]
+  const int nsets = n2p == n2 ? 1 : 2;
+  const int total = nsets * N1 * NP;
+  for (int o = threadIdx.x; o < total; o += NTH) {
+    const int k = o & (NP - 1);
+    const int rowi = o / NP, set = rowi / N1, n1 = rowi % N1;
+    const int n = (set ? n2p : n2) + N2 * n1;
+    if (n > NT / 2) continue;
+    const double2* q = Sh + (long long)n * S + 2 * p0;
+    const double2 x0 = __ldcs(q + k), x1 = __ldcs(q + k + NP);
+    const double2 E = cadd(x0, x1);
+    const double2 O = cmulc(csub(x0, x1), s_twx[k]);  // (x0 - x1) w^-k
+    sm[pad((2 * n1 + set) * NP + k)] = make_double2(E.x - O.y, E.y + O.x);
+    if (n != 0 && n != NT / 2) {
+      const int m = NT - n;
+      const int setp = (m % N2) == n2 ? 0 : 1, n1p = m / N2;
+      sm[pad((2 * n1p + setp) * NP + ((NP - k) & (NP - 1)))] = make_double2(E.x + O.y, O.x - E.y);
+    }
+  }
+  __syncthreads();
+  // (1) NP-point inverse FFTs over p of the 16 rows, in place
+  fft_io<NP, 2 * N1, true, true, NTH, true, true, kRX>(
+      sm, s_twp,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(NP, kRX);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = sm[pad(c * NP + j + m * s)];
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(NP, kRX);
+#pragma unroll
+        for (int m = 0; m < RL; ++m) sm[pad(c * NP + j + m * s)] = w[m];
+      });
+  __syncthreads();
+  // (2) N1-point inverse DFTs over n1 of the sequences (set, p), twiddle, out to W[n2][t1][pair]
+  fft_io<N1, C, true, false, NTH, true, false, kRM>(
+      sm, s_twp,
+      [&](int, auto, int c, double2* v) {
+        const int set = c < NP ? 0 : 1, pc = c & (NP - 1);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = sm[pad((2 * m + set) * NP + pc)];
+      },
+      [&](int, auto, int c, const double2* w) {
+        const int set = c < NP ? 0 : 1, pc = c & (NP - 1);
+        if (set == 1 && nsets == 1) return;  // duplicate of the self-partnered residue
+        const int rr = set ? n2p : n2;
+        const double2* tws = set ? s_twb : s_twa;
+        double2* q = W + (long long)rr * N1 * Pc + pl0 + pc;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) __stcg(q + (long long)m * Pc, cmul(w[m], tws[m]));
+      });
+}
+
+template <int NT, int NX>
+void set_attrs() {
+  using F = Fx<NT, NX>;
+  static bool done = false;
+  if (done) return;
+  constexpr int N2 = F::N2, KP = F::KP;
+  const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
+  cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, true, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, false, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tfx_fwd_s2<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_inv_s1<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 1, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, false, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, false, 1, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  done = true;
+}
+
+template <int NT, int NX>
+cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
+                const double2* twx, double2* scratch, long long chunk_pairs, cudaStream_t st, int* nl) {
+  using F = Fx<NT, NX>;
+  constexpr int N2 = F::N2, KP = F::KP, NP = F::NP;
+  set_attrs<NT, NX>();
+  const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
+  const bool vec = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
+  const long long npairs = S / 2;
+  int n = 0;
+  for (long long p = 0; p < npairs; p += chunk_pairs) {
+    const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
+    const dim3 g1((unsigned)((pc + KP - 1) / KP), kN1), g2((unsigned)(pc / NP), N2 / 2 + 1);
+    if (vec)
+      tf4_fwd_s1<NT, N2, KP, true, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+    else
+      tf4_fwd_s1<NT, N2, KP, false, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+    tfx_fwd_s2<NT, NX><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, Sh, twx);
+    n += 2;
+  }
+  *nl = n;
+  return cudaGetLastError();
+}
+
+template <int NT, int NX>
+cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
+                const double2* twx, double2* scratch, long long chunk_pairs, int accumulate, cudaStream_t st,
+                int* nl) {
+  using F = Fx<NT, NX>;
+  constexpr int N2 = F::N2, KP = F::KP, NP = F::NP;
+  set_attrs<NT, NX>();
+  const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
+  const bool vec = (reinterpret_cast<uintptr_t>(z) & 15) == 0;
+  const long long npairs = S / 2;
+  int n = 0;
+  for (long long p = 0; p < npairs; p += chunk_pairs) {
+    const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
+    const dim3 g1((unsigned)(pc / NP), N2 / 2 + 1), g2((unsigned)((pc + KP - 1) / KP), kN1);
+    tfx_inv_s1<NT, NX><<<g1, F::NTH, sm2, st>>>(Sh, S, p, pc, scratch, twx, tb.twt);
+    const int th = KP * N2 / kRS;
+    if (vec) {
+      if (accumulate)
+        tf4_inv_s2<NT, N2, KP, true, 1, kRS><<<g2, th, sm1, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+      else
+        tf4_inv_s2<NT, N2, KP, true, 0, kRS><<<g2, th, sm1, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+    } else {
+      if (accumulate)
+        tf4_inv_s2<NT, N2, KP, false, 1, kRS><<<g2, th, sm1, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+      else
+        tf4_inv_s2<NT, N2, KP, false, 0, kRS><<<g2, th, sm1, st>>>(scratch, S, p, pc, z, igam, tb.tw2);
+    }
+    n += 2;
+  }
+  *nl = n;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Nt <= 512: the single-tile time FFT plus the three-launch slab solve measured faster on B200 (cfg3)
+int pd_tfx_supported(int nt, int nx) {
+  const bool t = nt == 1024 || nt == 2048 || nt == 4096;
+  const bool x = nx == 32 || nx == 64 || nx == 128 || nx == 256 || nx == 512 || nx == 1024;
+  return t && x;
+}
+int pd_tfx_n2(int nt) { return nt / kN1; }
+long long pd_tfx_chunk_align(int nt, int nx) {
+  const long long kp = 4096 / (nt / kN1) < 8 ? 8 : 4096 / (nt / kN1);
+  const long long np = nx / 2;
+  return kp > np ? kp : np;
+}
+
+#define PD_TFX_ROW(T, FN, ARGS)                                                                      \
+  case T * 10000 + 32: return FN<T, 32> ARGS;                                                       \
+  case T * 10000 + 64: return FN<T, 64> ARGS;                                                       \
+  case T * 10000 + 128: return FN<T, 128> ARGS;                                                     \
+  case T * 10000 + 256: return FN<T, 256> ARGS;                                                     \
+  case T * 10000 + 512: return FN<T, 512> ARGS;                                                     \
+  case T * 10000 + 1024: return FN<T, 1024> ARGS;
+#define PD_TFX_SWITCH(FN, ARGS)                                                                      \
+  switch (nt * 10000 + nx) {                                                                         \
+    PD_TFX_ROW(1024, FN, ARGS) PD_TFX_ROW(2048, FN, ARGS) PD_TFX_ROW(4096, FN, ARGS)                 \
+    default: return cudaErrorInvalidValue;                                                           \
+  }
+
+cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
+                              const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
+                              cudaStream_t st, int* nl) {
+  PD_TFX_SWITCH(fwd, (r, Sh, S, gam, tb, twx, scratch, chunk_pairs, st, nl))
+}
+
+cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
+                              const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
+                              int accumulate, cudaStream_t st, int* nl) {
+  PD_TFX_SWITCH(inv, (Sh, z, S, igam, tb, twx, scratch, chunk_pairs, accumulate, st, nl))
+}

@@ -34,6 +34,8 @@ SMALL = [
     (W.WAVE1D, W.LF, 31, 4), (W.WAVE1D, W.LF, 255, 512), (W.WAVE1D, W.LF, 4095, 64), (W.WAVE1D, W.LF, 100, 4096),
     (W.ADE2D, W.BE, 16, 2), (W.ADE2D, W.CN, 32, 64), (W.ADE2D, W.BE, 64, 16), (W.ADE2D, W.CN, 128, 8),
     (W.ADE2D, W.BE, 256, 4), (W.ADE2D, W.CN, 512, 2),
+    # time FFT with the x-FFT folded in (tfx.cu, Nt >= 1024): several x-rows per chunk, both residue cases
+    (W.ADE2D, W.BE, 32, 1024), (W.ADE2D, W.CN, 64, 1024), (W.ADE2D, W.CN, 32, 4096),
 ]
 
 

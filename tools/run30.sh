@@ -1,0 +1,2 @@
+for v in A B C D A B C D; do python tools/variant_apply.py tools/var/lib_$v.so cfg4 4; done
+for v in A B C D; do PD_NO_TFX=1 python tools/variant_apply.py tools/var/lib_$v.so cfg4 4; done

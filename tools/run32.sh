@@ -1,0 +1,3 @@
+timeout 1800 python -m pytest tests -m gpu -q -x -k "stationary or solve or tf4 or tfx or 4096 or 1024 or 2048" > gpurun_out/pytest32.log 2>&1; echo rc=$?; tail -2 gpurun_out/pytest32.log
+for c in cfg4 cfg2; do timeout 600 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/b32_$c.json 2>gpurun_out/b32_$c.err; python -c "
+import json; d=json.load(open('gpurun_out/b32_$c.json')); print('$c step', d['ms_per_step'], 'apply', d['apply']['ms']); print({k:(v['ms_per_call'],v['GBps']) for k,v in d['phases'].items()})"; done
