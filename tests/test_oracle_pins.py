@@ -14,7 +14,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 import workloads as W
-from oracle import dense, periodic, problems, solvers, spectral, stepping
+from oracle import dense, periodic, problems, solvers, spectral, stepping, tail
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -332,3 +332,53 @@ def test_residual_definitions():
     assert np.array_equal(solvers.residual(cfg, b, np.zeros_like(b)), b)
     u = dense.solve_A(cfg, b)
     assert np.linalg.norm(solvers.residual(cfg, b, u)) < 1e-12 * np.linalg.norm(b)
+
+
+# ------------------------------------------------------------------------------------------ O3 tail form (NEXT-1)
+TAIL_CASES = [W.CONFIGS[0], W.CONFIGS[1].scaled(nx=63, nt=64), W.CONFIGS[2].scaled(nx=31, nt=32),
+              W.CONFIGS[3].scaled(nx=16, ny=16, nt=16)]
+
+
+@pytest.mark.parametrize("cfg", TAIL_CASES, ids=lambda c: f"{c.op}-{c.scheme}")
+def test_tail_corner_is_P_minus_A(cfg):
+    """head_from_tail reproduces P_alpha - A from the plain matvecs (eq 1.1 vs eq 1.2): non-zero only in the first
+    H block rows, and there a function of the last H blocks only (H = 1 theta, 2 leapfrog)."""
+    H = tail.head_blocks(cfg)
+    assert H == (2 if cfg.scheme == W.LF else 1)
+    u = np.random.default_rng(1).standard_normal((cfg.nt, cfg.S))
+    d = problems.matvec_P(cfg, u) - problems.matvec_A(cfg, u)
+    assert np.abs(d[H:]).max() == 0.0
+    assert rel(tail.head_from_tail(cfg, u[cfg.nt - H:]), d[:H]) < 1e-12
+
+
+@pytest.mark.parametrize("cfg", TAIL_CASES, ids=lambda c: f"{c.op}-{c.scheme}")
+def test_tail_map_equals_last_blocks_of_full_apply(cfg):
+    """Economical Step (a) + truncated Step (c) (P:l.928-931) == last H blocks of O1 on the embedded vector."""
+    H = tail.head_blocks(cfg)
+    g = np.random.default_rng(2).standard_normal((H, cfg.S))
+    v = np.zeros((cfg.nt, cfg.S))
+    v[:H] = g
+    # both sides carry fp64 rounding amplified by up to Cond_2(V) <= 1/alpha (eq 2.13, reading t1)
+    assert rel(tail.tail_map(cfg, g), spectral.apply_precond(cfg, v)[cfg.nt - H:]) < max(1e-10, 1e-12 / cfg.alpha)
+
+
+@pytest.mark.parametrize("cfg", TAIL_CASES, ids=lambda c: f"{c.op}-{c.scheme}")
+def test_tail_solvers_same_iterates(cfg):
+    """[V6]: the tail-form stationary iteration and GMRES take the same number of iterations and return the same
+    u as the residual-form oracle solvers, for a head-supported b, a full-support b, a non-zero u0 and restarts."""
+    rng = np.random.default_rng(3)
+    b = problems.rhs(cfg, rng.standard_normal(cfg.S), rng.standard_normal(cfg.S) if cfg.scheme == W.LF else None)
+    u1, r1 = solvers.solve_stationary(cfg, b, tol=1e-10, maxit=30)
+    u2, r2 = tail.solve_stationary_tail(cfg, b, tol=1e-10, maxit=30)
+    assert (r1.iterations, r1.converged) == (r2.iterations, r2.converged)
+    assert rel(u2, u1) < 1e-11
+    bb = rng.standard_normal((cfg.nt, cfg.S))
+    u0 = rng.standard_normal((cfg.nt, cfg.S))
+    u1, r1 = solvers.solve_stationary(cfg, bb, u0=u0, tol=1e-10, maxit=40)
+    u2, r2 = tail.solve_stationary_tail(cfg, bb, u0=u0, tol=1e-10, maxit=40)
+    assert r1.iterations == r2.iterations and rel(u2, u1) < 1e-11
+    for rhs_, m in ((b, 5), (bb, 3)):
+        u1, r1 = solvers.solve_gmres(cfg, rhs_, tol=1e-10, m=m, maxit=40)
+        u2, r2 = tail.solve_gmres_tail(cfg, rhs_, tol=1e-10, m=m, maxit=40)
+        assert (r1.iterations, r1.converged) == (r2.iterations, r2.converged)
+        assert rel(u2, u1) < 1e-11
