@@ -134,6 +134,26 @@ PD_API pd_status pd_solve_stationary(pd_ctx* ctx, const double* b, double* u, do
  * Workspace for the basis ((m+1) vectors) is allocated on first use and kept by the context. */
 PD_API pd_status pd_solve_gmres(pd_ctx* ctx, const double* b, double* u, double tol, int m, int maxit, pd_report* rep);
 
+/* ---- waveform-relaxation tail form (oracle/tail.py) ----
+ * P_alpha - A is non-zero only between the first H time blocks (rows) and the last H blocks (columns),
+ * H = 1 for PD_BE / PD_CN and 2 for PD_LEAPFROG (alpha-corner of eq 1.2, P:l.80-84), so the iterations can
+ * carry only the "tail" of u between iterations (head-tail coupling of WR, P:l.762-773; economical Step (a),
+ * P:l.928-931).  Same iterates, iteration counts and stopping rule (||b - A u|| <= tol ||b||) as the
+ * residual-form solvers above; per iteration the work is the tail map below plus O(H S) vector operations
+ * instead of full passes over Nt x S.  Single-GPU contexts only (dist == NULL or size 1): PD_EINVAL otherwise;
+ * PD_EINVAL also when Nt < 2H.  Per-context tables (1D: F x H coefficients; 2D: the N x N transfer function
+ * tau, F N^2 divisions) are built on the first call and kept.
+ *
+ * pd_tail_map: tail = last H blocks of P_alpha^{-1} (E_H head), head and tail device [H][local dofs]
+ *   (must not alias).  Economical Step (a), Step (b) for every frequency, last H rows of Step (c). */
+PD_API pd_status pd_tail_map(pd_ctx* ctx, const double* head, double* tail);
+/* Stationary iteration (eq 5.1) in tail form; u: initial guess in, solution out (device [Nt][S]).
+ * rep->rel_residual = ||G (t^k - t^{k-1})|| / ||b|| = ||b - A u^k|| / ||b|| (P - A only touches the head). */
+PD_API pd_status pd_solve_stationary_tail(pd_ctx* ctx, const double* b, double* u, double tol, int maxit, pd_report* rep);
+/* Right-preconditioned restarted GMRES(m) in tail form: basis vectors a_j r0 + E_H h_j (a_j host, h_j device).
+ * Reports the true residual of the returned u (recomputed by the stencil at exit, as pd_solve_gmres). */
+PD_API pd_status pd_solve_gmres_tail(pd_ctx* ctx, const double* b, double* u, double tol, int m, int maxit, pd_report* rep);
+
 /* HOST-buffer variants for end-to-end use: copy the HOST input(s) to device workspace on the context
  * stream (pinned memory recommended), run, copy the HOST output back, synchronise. */
 PD_API pd_status pd_apply_precond_host(pd_ctx* ctx, const double* r_host, double* z_host);

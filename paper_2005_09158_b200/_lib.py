@@ -76,6 +76,9 @@ def load_library(path: str | None = None):
         "pd_build_rhs": (ip, [vp, vp, vp, vp, vp]),
         "pd_solve_stationary": (ip, [vp, vp, vp, C.c_double, ip, C.POINTER(pd_report)]),
         "pd_solve_gmres": (ip, [vp, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
+        "pd_tail_map": (ip, [vp, vp, vp]),
+        "pd_solve_stationary_tail": (ip, [vp, vp, vp, C.c_double, ip, C.POINTER(pd_report)]),
+        "pd_solve_gmres_tail": (ip, [vp, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_apply_precond_host": (ip, [vp, vp, vp]),
         "pd_solve_host": (ip, [vp, ip, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_kernel_launches": (C.c_longlong, [vp]),
@@ -163,6 +166,7 @@ class ParaDiag:
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = pd_dist(rank, size, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
         self.rank, self.size = rank, size
+        self.scheme = scheme
         ctx = C.c_void_p()
         st = self._lib.pd_setup(C.byref(g), dt, nt, alpha, scheme, C.byref(d),
                                 C.c_void_p(self.stream.cuda_stream), C.byref(ctx))
@@ -247,6 +251,36 @@ class ParaDiag:
         u = torch.zeros(self.shape, dtype=torch.float64, device="cuda") if u is None else u
         rep, hist = self._report(maxit + 2)
         st = self._lib.pd_solve_gmres(self._ctx, _ptr(b), _ptr(u), tol, m, maxit, C.byref(rep))
+        if raise_on_fail:
+            _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
+        return u, self._mk(st, rep, hist)
+
+    # ---- WR tail form (include/paradiag.h; same iterates as the two solvers above) ----
+    @property
+    def head_blocks(self) -> int:
+        return 2 if self.scheme == LEAPFROG else 1
+
+    def tail_map(self, head, tail=None):
+        """tail = last H blocks of P^{-1}(E_H head); head, tail: [H, S] device float64."""
+        import torch
+        tail = torch.empty_like(head) if tail is None else tail
+        _check(self._lib, self._ctx, self._lib.pd_tail_map(self._ctx, _ptr(head), _ptr(tail)))
+        return tail
+
+    def solve_stationary_tail(self, b, u=None, tol=1e-10, maxit=100, raise_on_fail=True):
+        import torch
+        u = torch.zeros(self.shape, dtype=torch.float64, device="cuda") if u is None else u
+        rep, hist = self._report(maxit + 2)
+        st = self._lib.pd_solve_stationary_tail(self._ctx, _ptr(b), _ptr(u), tol, maxit, C.byref(rep))
+        if raise_on_fail:
+            _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
+        return u, self._mk(st, rep, hist)
+
+    def solve_gmres_tail(self, b, u=None, tol=1e-10, m=20, maxit=100, raise_on_fail=True):
+        import torch
+        u = torch.zeros(self.shape, dtype=torch.float64, device="cuda") if u is None else u
+        rep, hist = self._report(maxit + 2)
+        st = self._lib.pd_solve_gmres_tail(self._ctx, _ptr(b), _ptr(u), tol, m, maxit, C.byref(rep))
         if raise_on_fail:
             _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
         return u, self._mk(st, rep, hist)

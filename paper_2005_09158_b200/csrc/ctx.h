@@ -104,6 +104,21 @@ struct pd_ctx {
   std::vector<GraphEntry> graphs;
   bool use_graphs = false;
   cudaStream_t cap_stream = nullptr;  // private stream for capture (the legacy stream cannot capture)
+  // WR tail form (tailform.cpp), built on first use
+  struct TailState {
+    bool ready = false;
+    int H = 0, G = 0;
+    pd_tail_g gc{};
+    double2* hc = nullptr;    // 1D: [F][H] economical Step (a) coefficients
+    double2* ow = nullptr;    // 1D: [F][H] Step (c) weights of the last H rows (with multiplicity)
+    double* part = nullptr;   // 1D: [G][H][S] per-CTA partial sums
+    double2* tau = nullptr;   // 2D: [N][N] transfer function
+    double2* work = nullptr;  // 2D: [N][N] complex slab
+    std::vector<double*> scr;  // head-sized scratch vectors
+    std::vector<double*> Vh;   // reduced GMRES basis (heads)
+    int* flag = nullptr;       // device flag (any non-zero)
+    int* hflag = nullptr;      // pinned host copy
+  } tail;
   // diagnostics
   long long launches = 0;
   bool timing = false;
@@ -137,7 +152,13 @@ void pd_dist_free(pd_ctx* c);
 pd_status pd_dist_apply(pd_ctx* c, const double* r, double* z, int accumulate);
 pd_status pd_dist_stencil(pd_ctx* c, const double* b, const double* u, double* out, double* norm2_dev_partial_sum);
 pd_status pd_dist_build_rhs(pd_ctx* c, const double* u0, const double* v0, const double* f, double* b);
-// paradiag.cpp helpers used by dist.cpp
+// paradiag.cpp helpers used by dist.cpp and tailform.cpp
+pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate);
+pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2);
+pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a, double* y,
+                      long long n, double* host_out);
+extern "C" void pd_report_push(pd_report* rep, double v);
+void pd_tail_free(pd_ctx* c);
 pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0);
 pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S);
 pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate);

@@ -41,6 +41,10 @@ cudaError_t pd_launch_tridiag(double2* Sh, int nx, int nfreq, const pd_tri_coef*
                               cudaStream_t st);
 int pd_tridiag_rows_per_thread();
 int pd_tridiag_threads(int nx);
+// WR tail form (tridiag.cu): per-CTA partial sums part[G][H][nx] of sum_n Re(ow[n][a] x_n), x_n the solve of
+// frequency n with right-hand side sum_t hc[n][t] g_t (g: [H][nx] real); G CTAs stride over the nfreq frequencies.
+cudaError_t pd_launch_tail1d(const double* g, double* part, int G, int nx, int nfreq, int H, const pd_tri_coef* coef,
+                             const double2* hc, const double2* ow, cudaStream_t st);
 
 // ---- Steps (a)/(c), 2D periodic, with the x-FFT of Step (b) folded in (tfx.cu): N1 = 8, N2 = Nt/8 ----
 // The spectrum then holds X_n[y][kx]; Step (b) runs only the slab column pass (pd_launch_slab2d cols_only).
@@ -65,6 +69,8 @@ struct pd_slab_params {
 int pd_slab2d_supported(int n);
 int pd_slab2d_chunk(int n, int nfreq);
 // chunk = slabs per L2-resident chunk; *launches = kernels launched
+// one N x N complex slab in place: 2D FFT, multiply by tab[ky*N + kx] / N^2, inverse 2D FFT (tail map, tail.cu)
+cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, const double2* tw, cudaStream_t st);
 cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                              const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
                              int chunk, int cols_only, cudaStream_t st, int* launches);
@@ -103,3 +109,18 @@ cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coe
 cudaError_t pd_launch_reduce_partials(const double* partial, int nblk, int k, double* out, cudaStream_t st);
 // y = a x + b y
 cudaError_t pd_launch_axpby(double* y, const double* x, double a, double b, long long n, cudaStream_t st);
+
+// WR tail form (tail.cu): (P - A) head-from-tail coefficients, H <= 2 blocks
+struct pd_tail_g {
+  int H;
+  double pI[2][2], pK[2][2];  // head_a = sum_b pI[a][b] tail_b + pK[a][b] K tail_b
+};
+cudaError_t pd_launch_head_G(const pd_stencil& p, const pd_tail_g& gc, const double* tail, double* head, long long S,
+                             cudaStream_t st);
+cudaError_t pd_launch_reduce_rows(const double* part, int G, long long len, double* out, cudaStream_t st);
+cudaError_t pd_launch_tau2d(double2* tau, int n, int nfreq, const double2* lam1, const double2* lam2, const double2* w,
+                            const double* sx, const double* sn, pd_slab_params prm, cudaStream_t st);
+cudaError_t pd_launch_r2c(const double* g, double2* z, long long n, cudaStream_t st);
+cudaError_t pd_launch_take_real(const double2* z, double* out, long long n, cudaStream_t st);
+// *flag = 1 if any x[i] != 0 (i < n), else unchanged (caller zeroes it)
+cudaError_t pd_launch_any_nonzero(const double* x, long long n, int* flag, cudaStream_t st);

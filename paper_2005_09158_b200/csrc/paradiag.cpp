@@ -123,6 +123,7 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
 
 static void free_ctx(pd_ctx* c) {
   if (!c) return;
+  pd_tail_free(c);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
   for (void* p : ptrs)
@@ -540,7 +541,7 @@ static pd_status apply_direct(pd_ctx* c, const double* r, double* z, int accumul
 
 // z = P^{-1} r, or u += P^{-1} r when accumulate.  With graphs enabled (single GPU, phase timing off) the
 // launch sequence of each (r, z, accumulate) triple is captured once and replayed as one CUDA graph.
-static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
+pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
   if (!c->use_graphs || c->dist_mode != 0 || c->timing) return apply_direct(c, r, z, accumulate);
   for (auto& g : c->graphs)
     if (g.r == r && g.z == z && g.acc == accumulate) {
@@ -573,7 +574,7 @@ static pd_status apply_impl(pd_ctx* c, const double* r, double* z, int accumulat
 }
 
 // out = b - A u (b != NULL) or A u; if norm2 != NULL: deterministic ||out||^2 into *norm2 (host, syncs)
-static pd_status stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2) {
+pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2) {
   const int ph = b ? 3 : 5;
   phase_begin(c, ph);
   if (c->dist_mode != 0) {
@@ -597,9 +598,8 @@ static pd_status stencil_impl(pd_ctx* c, const double* b, const double* u, doubl
 
 // Krylov sweep (blas1.cu) over the local vector; the k (or 1) reduced values all-reduced across ranks and
 // copied to host_out (syncs) unless host_out == NULL (mode 3)
-static pd_status krylov_impl(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a,
-                             double* y, double* host_out) {
-  const long long n = (long long)c->nt * c->S;
+pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a, double* y,
+                      long long n, double* host_out) {
   phase_begin(c, 6);
   PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st));
   if (mode != 3) {
@@ -617,6 +617,11 @@ static pd_status krylov_impl(pd_ctx* c, int mode, const double* const* X, const 
   return PD_OK;
 }
 
+static pd_status krylov_impl(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a,
+                             double* y, double* host_out) {
+  return pd_krylov_n(c, mode, X, coef, k, a, y, (long long)c->nt * c->S, host_out);
+}
+
 // dots[i] = <X[i], y>
 static pd_status dots_impl(pd_ctx* c, const double* const* X, int k, const double* y, double* host_out) {
   return krylov_impl(c, 0, X, nullptr, k, 0.0, const_cast<double*>(y), host_out);
@@ -626,17 +631,17 @@ extern "C" {
 
 pd_status pd_apply_precond(pd_ctx* c, const double* r, double* z) {
   if (!c || !r || !z) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
-  return apply_impl(c, r, z, 0);
+  return pd_apply_impl(c, r, z, 0);
 }
 
 pd_status pd_residual(pd_ctx* c, const double* b, const double* u, double* r, double* rnorm2_host) {
   if (!c || !b || !u || !r) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
-  return stencil_impl(c, b, u, r, rnorm2_host);
+  return pd_stencil_impl(c, b, u, r, rnorm2_host);
 }
 
 pd_status pd_matvec(pd_ctx* c, const double* u, double* w) {
   if (!c || !u || !w) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
-  return stencil_impl(c, nullptr, u, w, nullptr);
+  return pd_stencil_impl(c, nullptr, u, w, nullptr);
 }
 
 pd_status pd_build_rhs(pd_ctx* c, const double* u0, const double* v0, const double* f, double* b) {
@@ -646,7 +651,7 @@ pd_status pd_build_rhs(pd_ctx* c, const double* u0, const double* v0, const doub
   return PD_OK;
 }
 
-static void report_push(pd_report* rep, double v) {
+void pd_report_push(pd_report* rep, double v) {
   if (rep && rep->history && rep->history_len < rep->history_cap) rep->history[rep->history_len] = v;
   if (rep) rep->history_len++;
 }
@@ -670,12 +675,12 @@ pd_status pd_solve_stationary(pd_ctx* c, const double* b, double* u, double tol,
   double rel = 0;
   for (;;) {
     double rr = 0;
-    s = stencil_impl(c, b, u, c->rvec, &rr);  // r = b - A u (eq 5.1)
+    s = pd_stencil_impl(c, b, u, c->rvec, &rr);  // r = b - A u (eq 5.1)
     if (s != PD_OK) return s;
     rel = std::sqrt(rr) / bnorm;
-    if (k > 0) report_push(rep, rel);
+    if (k > 0) pd_report_push(rep, rel);
     if (rel <= tol || k >= maxit) break;
-    s = apply_impl(c, c->rvec, u, 1);  // u += P^{-1} r (fused into Step (c))
+    s = pd_apply_impl(c, c->rvec, u, 1);  // u += P^{-1} r (fused into Step (c))
     if (s != PD_OK) return s;
     ++k;
   }
@@ -729,7 +734,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
   }
   // Basis kept scaled: V_i = sc[i] * X_i with X_i = c->V[i] in memory, so normalising costs no sweep.
   double rr = 0;
-  s = stencil_impl(c, b, u, c->V[0], &rr);  // X_0 = r = b - A u
+  s = pd_stencil_impl(c, b, u, c->V[0], &rr);  // X_0 = r = b - A u
   if (s != PD_OK) return s;
   double beta = std::sqrt(rr);
   int its = 0;
@@ -744,11 +749,11 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     int kk = 0;
     for (int j = 0; j < m; ++j) {
       // w_raw = A P^{-1} X_j;  true w = sc[j] * w_raw
-      s = apply_impl(c, c->V[j], c->zvec, 0);
+      s = pd_apply_impl(c, c->V[j], c->zvec, 0);
       if (s != PD_OK) return s;
       ++its;
       double* w = c->V[j + 1];
-      s = stencil_impl(c, nullptr, c->zvec, w, nullptr);
+      s = pd_stencil_impl(c, nullptr, c->zvec, w, nullptr);
       if (s != PD_OK) return s;
       // CGS2: h_i = <V_i, w> = sc_i sc_j <X_i, w_raw>;  w_raw -= sum (h_i sc_i / sc_j) X_i  (fused with 2nd dots)
       s = krylov_impl(c, 0, Xp, nullptr, j + 1, 0.0, w, h.data());
@@ -783,7 +788,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
       gv[j + 1] = -sn[j] * gv[j];
       gv[j] = cs[j] * gv[j];
       kk = j + 1;
-      report_push(rep, std::fabs(gv[j + 1]) / bnorm);
+      pd_report_push(rep, std::fabs(gv[j + 1]) / bnorm);
       if (std::fabs(gv[j + 1]) <= tol * bnorm || its >= maxit) break;
       if (hn == 0.0) {
         breakdown = true;
@@ -800,9 +805,9 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     for (int i = 0; i < kk; ++i) coef[i] = y[i] * sc[i];
     s = krylov_impl(c, 3, Xp, coef.data(), kk, 0.0, c->zvec, nullptr);
     if (s != PD_OK) return s;
-    s = apply_impl(c, c->zvec, u, 1);
+    s = pd_apply_impl(c, c->zvec, u, 1);
     if (s != PD_OK) return s;
-    s = stencil_impl(c, b, u, c->V[0], &rr);  // true residual, also the restart vector X_0
+    s = pd_stencil_impl(c, b, u, c->V[0], &rr);  // true residual, also the restart vector X_0
     if (s != PD_OK) return s;
     beta = std::sqrt(rr);
     conv = beta <= tol * bnorm;
@@ -833,7 +838,7 @@ pd_status pd_apply_precond_host(pd_ctx* c, const double* rh, double* zh) {
   if (s != PD_OK) return s;
   const size_t bytes = sizeof(double) * c->nt * c->S;
   PD_CUDA(c, cudaMemcpyAsync(c->stage_a, rh, bytes, cudaMemcpyHostToDevice, c->st));
-  s = apply_impl(c, c->stage_a, c->stage_b, 0);
+  s = pd_apply_impl(c, c->stage_a, c->stage_b, 0);
   if (s != PD_OK) return s;
   PD_CUDA(c, cudaMemcpyAsync(zh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
   PD_CUDA(c, cudaStreamSynchronize(c->st));

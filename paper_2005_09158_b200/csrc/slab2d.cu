@@ -67,12 +67,13 @@ slab_rows_kernel(double2* __restrict__ base, const double2* __restrict__ tw) {
       });
 }
 
-// columns [c0, c0 + C) of slab (slab0 + blockIdx.y): forward FFT along y, divide, inverse FFT along y
-template <int N>
+// columns [c0, c0 + C) of slab (slab0 + blockIdx.y): forward FFT along y, divide, inverse FFT along y.
+// FILTER: multiply by tab[ky*N + kx] instead of dividing by lambda1 + lambda2 kappa (the WR tail map, tail.cu).
+template <int N, bool FILTER = false>
 __global__ void __launch_bounds__(ColCfg<N>::NTH, ColCfg<N>::MINB)
 slab_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict__ lam1,
                  const double2* __restrict__ lam2, const double* __restrict__ sx, const double* __restrict__ sn,
-                 pd_slab_params prm, const double2* __restrict__ tw) {
+                 pd_slab_params prm, const double2* __restrict__ tw, const double2* __restrict__ tab = nullptr) {
   using T = ColCfg<N>;
   constexpr int C = T::C, NTH = T::NTH, RM = T::RM, R0 = first_radix(N, RM), RL = last_radix(N, RM);
   extern __shared__ double2 sm[];
@@ -80,7 +81,7 @@ slab_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict_
   const int n = slab0 + blockIdx.y;
   const int c0 = blockIdx.x * C;
   double2* slab = Sh + (long long)n * N * N + c0;
-  const double2 l1 = lam1[n], l2 = lam2[n];
+  const double2 l1 = FILTER ? czero() : lam1[n], l2 = FILTER ? czero() : lam2[n];
   const double invNN = 1.0 / ((double)N * (double)N);
   load_table(s_tw, tw, N);
   __syncthreads();
@@ -96,8 +97,14 @@ slab_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict_
       [&](int j, auto st, int c, const double2* w) {
         constexpr int s = decltype(st)::value;
         const int kx = c0 + c;
-        const double ax = prm.kd * __ldg(sx + kx), bx = prm.cx * __ldg(sn + kx);
         const int a = lin<N, C, false>(j, c);
+        if constexpr (FILTER) {
+#pragma unroll
+          for (int m = 0; m < RL; ++m)
+            sm[soff<s * C>(a, m)] = cscale(cmul(w[m], __ldg(tab + (j + m * s) * N + kx)), invNN);
+          return;
+        }
+        const double ax = prm.kd * __ldg(sx + kx), bx = prm.cx * __ldg(sn + kx);
 #pragma unroll
         for (int m = 0; m < RL; ++m) {
           const int ky = j + m * s;
@@ -157,7 +164,41 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
   return cudaGetLastError();
 }
 
+template <int N>
+cudaError_t filter_n(double2* slab, const double2* tab, const double2* tw, cudaStream_t st) {
+  using T = SlabCfg<N>;
+  const int smem = smem_bytes<N>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(slab_rows_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(slab_cols_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  slab_rows_kernel<N, false><<<N / T::C, T::NTH, smem, st>>>(slab, tw);
+  slab_cols_kernel<N, true><<<dim3(N / T::C, 1), ColCfg<N>::NTH, smem, st>>>(slab, 0, nullptr, nullptr, nullptr,
+                                                                           nullptr, pd_slab_params{}, tw, tab);
+  slab_rows_kernel<N, true><<<N / T::C, T::NTH, smem, st>>>(slab, tw);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, const double2* tw, cudaStream_t st) {
+  switch (n) {
+    case 16: return filter_n<16>(slab, tab, tw, st);
+    case 32: return filter_n<32>(slab, tab, tw, st);
+    case 64: return filter_n<64>(slab, tab, tw, st);
+    case 128: return filter_n<128>(slab, tab, tw, st);
+    case 256: return filter_n<256>(slab, tab, tw, st);
+    case 512: return filter_n<512>(slab, tab, tw, st);
+    case 1024: return filter_n<1024>(slab, tab, tw, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 int pd_slab2d_supported(int n) { return n == 16 || n == 32 || n == 64 || n == 128 || n == 256 || n == 512 || n == 1024; }
 

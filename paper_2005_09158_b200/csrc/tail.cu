@@ -1,0 +1,122 @@
+// Kernels of the waveform-relaxation tail form (oracle/tail.py is the reference).
+//
+//   head_G:  (P_alpha - A) restricted to head rows x tail columns,
+//            head_a = sum_b (pI[a][b] tail_b + pK[a][b] K tail_b)   (alpha-corner of eq 1.2, P:l.80-84)
+//   reduce:  fixed-order sum of the per-CTA partials of the 1D tail map (tridiag.cu tail1d_kernel)
+//   tau2d:   2D periodic transfer function of the tail map (H = 1): with K diagonal in the 2D DFT basis
+//            (symbol kappa, reading c14), T(g) = Re IFFT2[ tau . FFT2(g) ],
+//              tau(kx, ky) = sum_{n < F} ow_n hc_n / (lambda_1n + lambda_2n kappa(kx, ky)),
+//            ow_n hc_n = m_n gamma_{Nt-1}^{-1} / Nt exp(2 pi i n (Nt-1) / Nt) (hc_n = gamma_0 = 1; m_n = half-spectrum
+//            multiplicity).  Computed once per context (F N^2 complex divisions, fixed order).
+//   r2c / take_real: real head <-> complex slab for the 2D filter (slab2d.cu pd_launch_slab2d_filter).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+__global__ void head_G_kernel(pd_stencil p, pd_tail_g gc, const double* __restrict__ tail, double* __restrict__ head,
+                              long long S) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < S; i += (long long)gridDim.x * blockDim.x) {
+    double kt[2] = {0.0, 0.0}, tv[2] = {0.0, 0.0};
+    for (int b = 0; b < gc.H; ++b) {
+      const double* t = tail + (long long)b * S;
+      tv[b] = t[i];
+      double k;
+      if (p.op == 2) {
+        const int nx = p.nx, ny = p.ny;
+        const int x = (int)(i % nx), y = (int)(i / nx);
+        const int xm = x == 0 ? nx - 1 : x - 1, xp = x == nx - 1 ? 0 : x + 1;
+        const int ym = y == 0 ? ny - 1 : y - 1, yp = y == ny - 1 ? 0 : y + 1;
+        k = p.k2c * tv[b] + p.k2x_m * t[(long long)y * nx + xm] + p.k2x_p * t[(long long)y * nx + xp] +
+            p.k2y_m * t[(long long)ym * nx + x] + p.k2y_p * t[(long long)yp * nx + x];
+      } else {
+        k = p.dia * tv[b] + (i > 0 ? p.sub * t[i - 1] : 0.0) + (i + 1 < S ? p.sup * t[i + 1] : 0.0);
+      }
+      kt[b] = k;
+    }
+    for (int a = 0; a < gc.H; ++a) {
+      double v = 0.0;
+      for (int b = 0; b < gc.H; ++b) v += gc.pI[a][b] * tv[b] + gc.pK[a][b] * kt[b];
+      head[(long long)a * S + i] = v;
+    }
+  }
+}
+
+__global__ void reduce_rows_kernel(const double* __restrict__ part, int G, long long len, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s += part[(long long)g * len + i];
+    out[i] = s;
+  }
+}
+
+__global__ void tau2d_kernel(double2* __restrict__ tau, int N, int F, const double2* __restrict__ lam1,
+                             const double2* __restrict__ lam2, const double2* __restrict__ w,
+                             const double* __restrict__ sx, const double* __restrict__ sn, pd_slab_params prm) {
+  const long long NN = (long long)N * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NN; i += (long long)gridDim.x * blockDim.x) {
+    const int kx = (int)(i % N), ky = (int)(i / N);
+    const double2 kap = make_double2(prm.kd * (sx[kx] + sx[ky]), prm.cx * sn[kx] + prm.cy * sn[ky]);
+    double2 acc = czero();
+    for (int n = 0; n < F; ++n) acc = cadd(acc, cdiv(w[n], cfma(lam2[n], kap, lam1[n])));
+    tau[i] = acc;
+  }
+}
+
+__global__ void r2c_kernel(const double* __restrict__ g, double2* __restrict__ z, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    z[i] = make_double2(g[i], 0.0);
+}
+
+__global__ void take_real_kernel(const double2* __restrict__ z, double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = z[i].x;
+}
+
+__global__ void any_nonzero_kernel(const double* __restrict__ x, long long n, int* flag) {
+  bool nz = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    nz |= x[i] != 0.0;
+  if (__syncthreads_or(nz) && threadIdx.x == 0) *flag = 1;
+}
+
+unsigned grid_for(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t pd_launch_head_G(const pd_stencil& p, const pd_tail_g& gc, const double* tail, double* head, long long S,
+                             cudaStream_t st) {
+  head_G_kernel<<<grid_for(S, 256), 256, 0, st>>>(p, gc, tail, head, S);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_reduce_rows(const double* part, int G, long long len, double* out, cudaStream_t st) {
+  reduce_rows_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, G, len, out);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_tau2d(double2* tau, int n, int nfreq, const double2* lam1, const double2* lam2, const double2* w,
+                            const double* sx, const double* sn, pd_slab_params prm, cudaStream_t st) {
+  tau2d_kernel<<<grid_for((long long)n * n, 128), 128, 0, st>>>(tau, n, nfreq, lam1, lam2, w, sx, sn, prm);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_r2c(const double* g, double2* z, long long n, cudaStream_t st) {
+  r2c_kernel<<<grid_for(n, 256), 256, 0, st>>>(g, z, n);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_take_real(const double2* z, double* out, long long n, cudaStream_t st) {
+  take_real_kernel<<<grid_for(n, 256), 256, 0, st>>>(z, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_any_nonzero(const double* x, long long n, int* flag, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  any_nonzero_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
+}

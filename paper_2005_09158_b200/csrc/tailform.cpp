@@ -1,0 +1,382 @@
+// Waveform-relaxation "tail" form of the stationary iteration and of GMRES.
+// Reference implementation and derivation: oracle/tail.py (O3).  In brief (P:l.120-124, 762-773, 928-931):
+//   P_alpha - A touches only the first H time blocks (rows) and the last H blocks (columns), H = 1 for the
+//   theta-method and 2 for leapfrog:  (P - A) u = E_H G U_tail.  Hence
+//     stationary:  t^{k+1} = tail(P^{-1} b) + T(G t^k),  ||b - A u^k|| = ||G (t^k - t^{k-1})||,
+//                  u^k = P^{-1}(b + E_H G t^{k-1}) assembled once at exit;
+//     GMRES:       every Krylov vector is a r0 + E_H h, A P^{-1}(a r0 + E_H h) = a (r0 - E_H q0) + E_H (h - G T(h)),
+//                  q0 = G tail(P^{-1} r0); the basis is carried as (a_j on the host, h_j on the device).
+//   T(g) = tail(P^{-1}(E_H g)) is the tail map: the economical Step (a) (an H-term sum), the shifted solves of
+//   Step (b) for every frequency and only the last H rows of Step (c) - tridiag.cu tail1d_kernel in 1D, the
+//   transfer function tau in 2D (tail.cu).  Per iteration the work is O(H S) memory traffic plus the per-
+//   frequency solves (1D) instead of three full passes over Nt S dofs.
+// Single-GPU contexts only in this version (the sharded variant needs an H*S all-reduce).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "ctx.h"
+
+namespace {
+
+constexpr int kScr = 10;  // head-sized scratch vectors
+
+cudaError_t dalloc_d(double** p, size_t n) { return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 2) * sizeof(double)); }
+cudaError_t dalloc_c(double2** p, size_t n) { return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(double2)); }
+
+long long hs(const pd_ctx* c) { return (long long)c->tail.H * c->S; }
+
+pd_status tail_setup(pd_ctx* c) {
+  auto& T = c->tail;
+  if (T.ready) return PD_OK;
+  if (c->dist_mode != 0) return fail(c, PD_EINVAL, "tail form: single-GPU contexts only");
+  const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
+  if (c->nt < 2 * H) return fail(c, PD_EINVAL, "tail form needs Nt >= %d", 2 * H);
+  const int nt = c->nt, F = c->F;
+  const double dt = c->dt, al = c->alpha;
+  // time first columns (oracle problems.time_first_columns): taps 0..2
+  double c1[3] = {0, 0, 0}, c2[3] = {0, 0, 0};
+  if (c->scheme == PD_LEAPFROG) {
+    c1[0] = 1.0 / (dt * dt); c1[1] = -2.0 / (dt * dt); c1[2] = 1.0 / (dt * dt);
+    c2[0] = 0.5; c2[2] = 0.5;
+  } else {
+    const double th = c->scheme == PD_BE ? 1.0 : 0.5;
+    c1[0] = 1.0 / dt; c1[1] = -1.0 / dt;
+    c2[0] = th; c2[1] = 1.0 - th;
+  }
+  // alpha-corner of the alpha-circulants: entry (a, j) with a < j, j = Nt-H+b, tap k = a - j + Nt = a - b + H
+  T.gc = pd_tail_g{};
+  T.gc.H = H;
+  for (int a = 0; a < H; ++a)
+    for (int b = 0; b < H; ++b) {
+      const int j = nt - H + b, k = a - b + H;
+      if (a < j && k >= 1 && k <= 2) {
+        T.gc.pI[a][b] = al * c1[k];
+        T.gc.pK[a][b] = al * c2[k];
+      }
+    }
+  // economical Step (a) coefficients and last-H-row Step (c) weights (long double, closed form)
+  typedef std::complex<long double> cld;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  std::vector<double2> hc((size_t)F * H), ow((size_t)F * H), w2((size_t)F);
+  for (int n = 0; n < F; ++n) {
+    const long double mult = (n == 0 || 2 * n == nt) ? 1.0L : 2.0L;
+    for (int t = 0; t < H; ++t) {
+      const long double g = powl((long double)al, (long double)t / nt);
+      const cld v = g * std::exp(cld(0.0L, -2.0L * pi * n * t / nt));
+      hc[(size_t)n * H + t] = make_double2((double)v.real(), (double)v.imag());
+    }
+    for (int a = 0; a < H; ++a) {
+      const int t = nt - H + a;
+      const long double ig = powl((long double)al, -(long double)t / nt);
+      const cld v = mult * ig / (long double)nt * std::exp(cld(0.0L, 2.0L * pi * n * t / nt));
+      ow[(size_t)n * H + a] = make_double2((double)v.real(), (double)v.imag());
+    }
+    const cld wv = cld(ow[(size_t)n * H].x, ow[(size_t)n * H].y) * cld(hc[(size_t)n * H].x, hc[(size_t)n * H].y);
+    w2[n] = make_double2((double)wv.real(), (double)wv.imag());
+  }
+  const long long S = c->S;
+  if (c->g.op == PD_ADE2D_PERIODIC) {
+    const int N = c->g.nx;
+    double2* wd = nullptr;
+    PD_CUDA(c, dalloc_c(&wd, F));
+    PD_CUDA(c, cudaMemcpy(wd, w2.data(), F * sizeof(double2), cudaMemcpyHostToDevice));
+    PD_CUDA(c, dalloc_c(&T.tau, (size_t)N * N));
+    PD_CUDA(c, dalloc_c(&T.work, (size_t)N * N));
+    PD_LAUNCH(c, pd_launch_tau2d(T.tau, N, F, c->lam1, c->lam2, wd, c->sx, c->sn, c->slab, c->st));
+    PD_CUDA(c, cudaStreamSynchronize(c->st));
+    cudaFree(wd);
+  } else {
+    PD_CUDA(c, dalloc_c(&T.hc, (size_t)F * H));
+    PD_CUDA(c, dalloc_c(&T.ow, (size_t)F * H));
+    PD_CUDA(c, cudaMemcpy(T.hc, hc.data(), hc.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    PD_CUDA(c, cudaMemcpy(T.ow, ow.data(), ow.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    T.G = std::min(F, 4 * 148);
+    PD_CUDA(c, dalloc_d(&T.part, (size_t)T.G * H * S));
+  }
+  T.scr.assign(kScr, nullptr);
+  for (auto& p : T.scr) PD_CUDA(c, dalloc_d(&p, (size_t)H * S));
+  PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&T.flag), sizeof(int)));
+  PD_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&T.hflag), sizeof(int)));
+  T.H = H;
+  T.ready = true;
+  return PD_OK;
+}
+
+// out = T(g): last H blocks of P^{-1}(E_H g)   (g, out: [H][S], out must not alias g)
+pd_status tail_map(pd_ctx* c, const double* g, double* out) {
+  auto& T = c->tail;
+  const long long S = c->S;
+  if (c->g.op == PD_ADE2D_PERIODIC) {
+    PD_LAUNCH(c, pd_launch_r2c(g, T.work, S, c->st));
+    PD_CUDA(c, pd_launch_slab2d_filter(T.work, c->g.nx, T.tau, c->tw_s, c->st));
+    c->launches += 3;
+    PD_LAUNCH(c, pd_launch_take_real(T.work, out, S, c->st));
+  } else {
+    PD_LAUNCH(c, pd_launch_tail1d(g, T.part, T.G, c->g.nx, c->F, T.H, c->tri, T.hc, T.ow, c->st));
+    PD_LAUNCH(c, pd_launch_reduce_rows(T.part, T.G, (long long)T.H * S, out, c->st));
+  }
+  return PD_OK;
+}
+
+pd_status head_G(pd_ctx* c, const double* tail, double* head) {
+  PD_LAUNCH(c, pd_launch_head_G(c->sten, c->tail.gc, tail, head, c->S, c->st));
+  return PD_OK;
+}
+
+// true if any of x[0..n) is non-zero (syncs)
+pd_status any_nonzero(pd_ctx* c, const double* x, long long n, bool* out) {
+  auto& T = c->tail;
+  PD_CUDA(c, cudaMemsetAsync(T.flag, 0, sizeof(int), c->st));
+  PD_LAUNCH(c, pd_launch_any_nonzero(x, n, T.flag, c->st));
+  PD_CUDA(c, cudaMemcpyAsync(T.hflag, T.flag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  *out = *T.hflag != 0;
+  return PD_OK;
+}
+
+pd_status dots(pd_ctx* c, std::vector<const double*> X, const double* y, long long n, double* out) {
+  return pd_krylov_n(c, 0, X.data(), nullptr, (int)X.size(), 0.0, const_cast<double*>(y), n, out);
+}
+// y = sum c_i X_i (X may contain y)
+pd_status comb(pd_ctx* c, std::vector<const double*> X, std::vector<double> coef, double* y, long long n) {
+  return pd_krylov_n(c, 3, X.data(), coef.data(), (int)X.size(), 0.0, y, n, nullptr);
+}
+
+pd_status copy_tail(pd_ctx* c, const double* u, double* t) {
+  const long long S = c->S;
+  PD_CUDA(c, cudaMemcpyAsync(t, u + (long long)(c->nt - c->tail.H) * S, sizeof(double) * hs(c), cudaMemcpyDeviceToDevice,
+                             c->st));
+  return PD_OK;
+}
+
+pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {
+  PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * c->nt * c->S, c->st));
+  if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
+  return PD_OK;
+}
+
+#define PD_TRY(expr)              \
+  do {                            \
+    pd_status s_ = (expr);        \
+    if (s_ != PD_OK) return s_;   \
+  } while (0)
+
+}  // namespace
+
+void pd_tail_free(pd_ctx* c) {
+  auto& T = c->tail;
+  for (void* p : {(void*)T.hc, (void*)T.ow, (void*)T.part, (void*)T.tau, (void*)T.work, (void*)T.flag})
+    if (p) cudaFree(p);
+  for (double* p : T.scr) cudaFree(p);
+  for (double* p : T.Vh) cudaFree(p);
+  if (T.hflag) cudaFreeHost(T.hflag);
+  T = pd_ctx::TailState{};
+}
+
+extern "C" {
+
+pd_status pd_tail_map(pd_ctx* c, const double* head, double* tail) {
+  if (!c || !head || !tail) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  PD_TRY(tail_setup(c));
+  return tail_map(c, head, tail);
+}
+
+pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double tol, int maxit, pd_report* rep) {
+  if (!c || !b || !u) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  if (!(tol > 0) || maxit < 0) return fail(c, PD_EINVAL, "tol must be > 0, maxit >= 0");
+  PD_TRY(tail_setup(c));
+  const auto t0 = std::chrono::steady_clock::now();
+  if (rep) rep->history_len = 0;
+  auto& T = c->tail;
+  const long long n = (long long)c->nt * c->S, Hn = hs(c);
+  double bb = 0;
+  PD_TRY(pd_krylov_n(c, 0, &b, nullptr, 1, 0.0, const_cast<double*>(b), n, &bb));
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) return zero_report(c, u, rep);
+  double rr = 0;
+  PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // r^0 = b - A u^0
+  double rel = std::sqrt(rr) / bnorm;
+  int k = 0;
+  if (rel > tol && maxit > 0) {
+    double *tp = T.scr[0], *tc = T.scr[1], *yt = T.scr[2], *hd = T.scr[3], *dd = T.scr[4];
+    PD_TRY(copy_tail(c, u, tp));  // t^0
+    bool nonhead = true;
+    PD_TRY(any_nonzero(c, b + Hn, n - Hn, &nonhead));
+    if (nonhead) {
+      PD_TRY(pd_apply_impl(c, b, u, 0));  // u = y = P^{-1} b
+      PD_TRY(copy_tail(c, u, yt));
+    } else {
+      PD_TRY(tail_map(c, b, yt));  // b supported on the head: tail(P^{-1} b) = T(b_head)
+    }
+    for (;;) {
+      PD_TRY(head_G(c, tp, hd));
+      PD_TRY(tail_map(c, hd, tc));
+      PD_TRY(comb(c, {tc, yt}, {1.0, 1.0}, tc, Hn));  // t^{k+1} = y_tail + T(G t^k)
+      ++k;
+      PD_TRY(comb(c, {tc, tp}, {1.0, -1.0}, dd, Hn));
+      PD_TRY(head_G(c, dd, hd));                      // r^{k+1} = E_H G (t^{k+1} - t^k)
+      double h2 = 0;
+      PD_TRY(dots(c, {hd}, hd, Hn, &h2));
+      rel = std::sqrt(h2) / bnorm;
+      pd_report_push(rep, rel);
+      if (rel <= tol || k >= maxit) break;
+      std::swap(tp, tc);
+    }
+    // u^k = P^{-1}(b + E_H G t^{k-1})
+    PD_TRY(head_G(c, tp, hd));
+    PD_CUDA(c, cudaMemsetAsync(c->rvec, 0, sizeof(double) * n, c->st));
+    if (nonhead) {
+      PD_CUDA(c, cudaMemcpyAsync(c->rvec, hd, sizeof(double) * Hn, cudaMemcpyDeviceToDevice, c->st));
+      PD_TRY(pd_apply_impl(c, c->rvec, u, 1));  // u = y + P^{-1}(E_H G t^{k-1})
+    } else {
+      PD_TRY(comb(c, {b, hd}, {1.0, 1.0}, c->rvec, Hn));
+      PD_TRY(pd_apply_impl(c, c->rvec, u, 0));
+    }
+  }
+  const bool conv = rel <= tol;
+  if (rep) {
+    rep->iterations = k;
+    rep->converged = conv;
+    rep->rel_residual = rel;
+    rep->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return conv ? PD_OK : PD_NOT_CONVERGED;
+}
+
+pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol, int m, int maxit, pd_report* rep) {
+  if (!c || !b || !u) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  if (!(tol > 0) || maxit < 0 || m < 1 || m > 30) return fail(c, PD_EINVAL, "need tol > 0, maxit >= 0, 1 <= m <= 30");
+  PD_TRY(tail_setup(c));
+  const auto t0 = std::chrono::steady_clock::now();
+  if (rep) rep->history_len = 0;
+  auto& T = c->tail;
+  const long long n = (long long)c->nt * c->S, Hn = hs(c);
+  if ((int)T.Vh.size() < m + 1) {
+    for (double* p : T.Vh) cudaFree(p);
+    T.Vh.assign(m + 1, nullptr);
+    for (auto& p : T.Vh) PD_CUDA(c, dalloc_d(&p, (size_t)Hn));
+  }
+  if (!c->zvec) PD_CUDA(c, dalloc_d(&c->zvec, (size_t)n));
+  double bb = 0;
+  PD_TRY(pd_krylov_n(c, 0, &b, nullptr, 1, 0.0, const_cast<double*>(b), n, &bb));
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) return zero_report(c, u, rep);
+  double rr = 0;
+  PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // anchor r0 = b - A u0 (kept in rvec)
+  double beta = std::sqrt(rr);
+  int its = 0;
+  bool conv = beta <= tol * bnorm, breakdown = false;
+  double *q0 = T.scr[0], *tq = T.scr[1], *gt = T.scr[2], *w = T.scr[3], *ch = T.scr[4];
+  const double* r0h = c->rvec;  // head of the anchor
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), y(m), A(m + 1), Sd(m + 1), d(m + 2), d2(m + 2);
+  auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
+  while (!conv && its < maxit) {
+    bool nonhead = true;
+    PD_TRY(any_nonzero(c, c->rvec + Hn, n - Hn, &nonhead));
+    if (nonhead) {
+      PD_TRY(pd_apply_impl(c, c->rvec, c->zvec, 0));  // q0 = G tail(P^{-1} r0)
+      PD_TRY(copy_tail(c, c->zvec, tq));
+      PD_TRY(head_G(c, tq, q0));
+      A[0] = 1.0 / beta;
+      PD_CUDA(c, cudaMemsetAsync(T.Vh[0], 0, sizeof(double) * Hn, c->st));
+      Sd[0] = 0.0;
+    } else {
+      A[0] = 0.0;  // anchor supported on the head: carry it in h
+      PD_TRY(comb(c, {r0h}, {1.0 / beta}, T.Vh[0], Hn));
+      Sd[0] = beta;  // <h_0, r0h> = ||r0||^2 / beta
+    }
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int kk = 0;
+    for (int j = 0; j < m; ++j) {
+      // w = A P^{-1} v_j = (a_j, h_j - G T(h_j) - a_j q0)
+      PD_TRY(tail_map(c, T.Vh[j], tq));
+      PD_TRY(head_G(c, tq, gt));
+      if (nonhead)
+        PD_TRY(comb(c, {T.Vh[j], gt, q0}, {1.0, -1.0, -A[j]}, w, Hn));
+      else
+        PD_TRY(comb(c, {T.Vh[j], gt}, {1.0, -1.0}, w, Hn));
+      double wa = A[j];
+      ++its;
+      // CGS2 in the (a, h) representation: <x, y> = xa ya rr + xa <r0h, yh> + ya <xh, r0h> + <xh, yh>
+      std::vector<const double*> X(T.Vh.begin(), T.Vh.begin() + j + 1);
+      X.push_back(r0h);
+      std::vector<double> hsum(j + 1, 0.0);
+      PD_TRY(dots(c, X, w, Hn, d.data()));
+      for (int pass = 0; pass < 2; ++pass) {
+        const double e = d[j + 1];  // <r0h, w>
+        std::vector<double> coef(j + 2, 0.0);
+        double da = 0.0;
+        for (int i = 0; i <= j; ++i) {
+          const double hij = wa * A[i] * rr + wa * Sd[i] + A[i] * e + d[i];
+          hsum[i] += hij;
+          coef[i] = -hij;
+          da += hij * A[i];
+        }
+        wa -= da;
+        // w <- w - sum h_i h_i-vectors; partial dots of the updated w with X (next pass / norm)
+        PD_TRY(pd_krylov_n(c, 1, X.data(), coef.data(), j + 2, 1.0, w, Hn, d.data()));
+      }
+      double ww = 0;
+      PD_TRY(dots(c, {w}, w, Hn, &ww));
+      const double e = d[j + 1];
+      const double hn = std::sqrt(std::max(0.0, wa * wa * rr + 2.0 * wa * e + ww));
+      for (int i = 0; i <= j; ++i) Hs(i, j) = hsum[i];
+      Hs(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * Hs(i, j) + sn[i] * Hs(i + 1, j);
+        Hs(i + 1, j) = -sn[i] * Hs(i, j) + cs[i] * Hs(i + 1, j);
+        Hs(i, j) = t;
+      }
+      const double den = std::hypot(Hs(j, j), Hs(j + 1, j));
+      cs[j] = Hs(j, j) / den;
+      sn[j] = Hs(j + 1, j) / den;
+      Hs(j, j) = den;
+      Hs(j + 1, j) = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      kk = j + 1;
+      pd_report_push(rep, std::fabs(gv[j + 1]) / bnorm);
+      if (std::fabs(gv[j + 1]) <= tol * bnorm || its >= maxit) break;
+      if (hn == 0.0) {
+        breakdown = true;
+        break;
+      }
+      PD_TRY(comb(c, {w}, {1.0 / hn}, T.Vh[j + 1], Hn));
+      A[j + 1] = wa / hn;
+      Sd[j + 1] = e / hn;
+    }
+    for (int i = kk - 1; i >= 0; --i) {
+      double t = gv[i];
+      for (int l = i + 1; l < kk; ++l) t -= Hs(i, l) * y[l];
+      y[i] = t / Hs(i, i);
+    }
+    double ca = 0.0;
+    for (int i = 0; i < kk; ++i) ca += y[i] * A[i];
+    std::vector<const double*> Xc(T.Vh.begin(), T.Vh.begin() + kk);
+    PD_TRY(comb(c, Xc, std::vector<double>(y.begin(), y.begin() + kk), ch, Hn));
+    // u += P^{-1}(ca r0 + E_H ch): the anchor buffer becomes the right-hand side
+    PD_LAUNCH(c, pd_launch_axpby(c->rvec, c->rvec, ca, 0.0, n, c->st));
+    PD_TRY(comb(c, {c->rvec, ch}, {1.0, 1.0}, c->rvec, Hn));
+    PD_TRY(pd_apply_impl(c, c->rvec, u, 1));
+    PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // true residual; the next cycle's anchor
+    beta = std::sqrt(rr);
+    conv = beta <= tol * bnorm;
+    if (breakdown) break;
+  }
+  if (rep) {
+    rep->iterations = its;
+    rep->converged = conv;
+    rep->rel_residual = beta / bnorm;
+    rep->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  if (conv) return PD_OK;
+  if (breakdown) return fail(c, PD_EBREAKDOWN, "GMRES breakdown at iteration %d, residual %.3e", its, beta / bnorm);
+  return PD_NOT_CONVERGED;
+}
+
+}  // extern "C"

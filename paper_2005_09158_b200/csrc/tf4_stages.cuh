@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
         double* q = z + (long long)(t1 + N1 * j) * S + col;
         const long long step = (long long)N1 * s * S;
         const bool okx = VEC || col < S, oky = VEC || col + 1 < S;
+        (void)okx;
+        (void)oky;
         if constexpr (VEC && MODE) {
           // accumulate: issue all RL loads of the old values before the first store (no aliasing stall)
           double2 o[RL];
@@ -116,8 +118,7 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
             __stcs(reinterpret_cast<double2*>(q + m * step), make_double2(fma(g, w[m].x, o[m].x), fma(g, w[m].y, o[m].y)));
           }
           return;
-        }
-        if constexpr (!VEC && MODE) {
+        } else if constexpr (!VEC && MODE) {
           double ox[RL], oy[RL];
 #pragma unroll
           for (int m = 0; m < RL; ++m) {
@@ -131,17 +132,17 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
             if (oky) q[m * step + 1] = fma(g, w[m].y, oy[m]);
           }
           return;
-        }
+        } else {
 #pragma unroll
-        for (int m = 0; m < RL; ++m) {
-          const double g = s_g[j + m * s];
-          double* row = q + m * step;
-          if (VEC) {
-            double2* rp = reinterpret_cast<double2*>(row);
-            __stcs(rp, make_double2(g * w[m].x, g * w[m].y));
-          } else {
-            if (okx) row[0] = MODE ? fma(g, w[m].x, row[0]) : g * w[m].x;
-            if (oky) row[1] = MODE ? fma(g, w[m].y, row[1]) : g * w[m].y;
+          for (int m = 0; m < RL; ++m) {
+            const double g = s_g[j + m * s];
+            double* row = q + m * step;
+            if (VEC) {
+              __stcs(reinterpret_cast<double2*>(row), make_double2(g * w[m].x, g * w[m].y));
+            } else {
+              if (okx) row[0] = g * w[m].x;
+              if (oky) row[1] = g * w[m].y;
+            }
           }
         }
       });

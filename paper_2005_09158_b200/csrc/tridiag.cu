@@ -62,36 +62,27 @@ PD_D double2 block_affine_scan_excl(double2 e, double2 M, double2* tot) {
   return vl == 0 ? P : ex;
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT) tridiag_kernel(double2* __restrict__ Sh, int N, const pd_tri_coef* __restrict__ coef) {
-  constexpr int L = kL;
-  extern __shared__ double2 sbuf[];           // staging: NT*L + NT (padded rows)
-  __shared__ double2 R2POW[L], SPOW[L + 1], tot[NT / 32], bc[2];
-  const int n = blockIdx.x;
-  const pd_tri_coef cf = coef[n];
-  double2* row = Sh + (long long)n * N;
-
+// per-frequency tables in shared memory: R2POW[j] = r2^{j+1}, SPOW[j] = s^j (thread 0; caller synchronises)
+PD_D void tri_tables(const pd_tri_coef& cf, double2* R2POW, double2* SPOW) {
   if (threadIdx.x == 0) {
     double2 p = cf.r2, sp = make_double2(1.0, 0.0);
-    for (int j = 0; j < L; ++j) {
-      R2POW[j] = p;  // r2^{j+1}
+    for (int j = 0; j < kL; ++j) {
+      R2POW[j] = p;
       p = cmul(p, cf.r2);
-      SPOW[j] = sp;  // s^j
+      SPOW[j] = sp;
       sp = cmul(sp, cf.s);
     }
-    SPOW[L] = sp;
+    SPOW[kL] = sp;
   }
-  // coalesced load into padded staging: element i -> i + i/L
-  for (int i = threadIdx.x; i < N; i += NT) sbuf[i + i / L] = __ldcs(row + i);
-  __syncthreads();
+}
 
+// Solve the Toeplitz system for the rows this thread holds in registers (d: right-hand side in, x out).
+// Thread k owns rows [k*L, k*L + Lk).  All NT threads must call (block scans, barriers).
+template <int NT>
+PD_D void tri_solve_regs(double2 (&d)[kL], const pd_tri_coef& cf, int Lk, int i0, const double2* R2POW,
+                         const double2* SPOW, double2* tot, double2* bc) {
+  constexpr int L = kL;
   const int k = threadIdx.x;
-  const int i0 = k * L;
-  const int Lk = max(0, min(L, N - i0));
-  double2 d[L];
-#pragma unroll
-  for (int j = 0; j < L; ++j) d[j] = (j < Lk) ? sbuf[i0 + j + k] : czero();
-
   // forward local: w_j = r2 w_{j-1} + d_j (zero carry-in)
   double2 p = czero();
 #pragma unroll
@@ -142,12 +133,83 @@ __global__ void __launch_bounds__(NT) tridiag_kernel(double2* __restrict__ Sh, i
       d[j] = cfma(x0, q, d[j]);
     }
   }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) tridiag_kernel(double2* __restrict__ Sh, int N, const pd_tri_coef* __restrict__ coef) {
+  constexpr int L = kL;
+  extern __shared__ double2 sbuf[];           // staging: NT*L + NT (padded rows)
+  __shared__ double2 R2POW[L], SPOW[L + 1], tot[NT / 32], bc[2];
+  const int n = blockIdx.x;
+  const pd_tri_coef cf = coef[n];
+  double2* row = Sh + (long long)n * N;
+  tri_tables(cf, R2POW, SPOW);
+  // coalesced load into padded staging: element i -> i + i/L
+  for (int i = threadIdx.x; i < N; i += NT) sbuf[i + i / L] = __ldcs(row + i);
+  __syncthreads();
+
+  const int k = threadIdx.x;
+  const int i0 = k * L;
+  const int Lk = max(0, min(L, N - i0));
+  double2 d[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) d[j] = (j < Lk) ? sbuf[i0 + j + k] : czero();
+  tri_solve_regs<NT>(d, cf, Lk, i0, R2POW, SPOW, tot, bc);
   __syncthreads();  // staging buffer reuse
 #pragma unroll
   for (int j = 0; j < L; ++j)
     if (j < Lk) sbuf[i0 + j + k] = d[j];
   __syncthreads();
   for (int i = threadIdx.x; i < N; i += NT) __stcs(row + i, sbuf[i + i / L]);
+}
+
+// Tail map of the WR tail form (oracle/tail.py tail_map), 1D: for the frequencies
+// n = blockIdx.x, blockIdx.x + gridDim.x, ...: right-hand side sum_{t<H} hc[n][t] g_t (the economical Step (a)),
+// the Toeplitz solve of Step (b), and the last H rows of Step (c) as weighted sums Re(ow[n][a] x) accumulated in
+// registers (ow carries the half-spectrum multiplicity).  Per-CTA partial sums out: part[blockIdx.x][a][N].
+template <int NT, int H>
+__global__ void __launch_bounds__(NT) tail1d_kernel(const double* __restrict__ g, double* __restrict__ part, int N,
+                                                    int F, const pd_tri_coef* __restrict__ coef,
+                                                    const double2* __restrict__ hc, const double2* __restrict__ ow) {
+  constexpr int L = kL;
+  __shared__ double2 R2POW[L], SPOW[L + 1], tot[NT / 32], bc[2];
+  const int k = threadIdx.x;
+  const int i0 = k * L;
+  const int Lk = max(0, min(L, N - i0));
+  double acc[H][L];
+#pragma unroll
+  for (int a = 0; a < H; ++a)
+#pragma unroll
+    for (int j = 0; j < L; ++j) acc[a][j] = 0.0;
+  for (int n = blockIdx.x; n < F; n += gridDim.x) {
+    const pd_tri_coef cf = coef[n];
+    __syncthreads();  // previous frequency's tables consumed
+    tri_tables(cf, R2POW, SPOW);
+    __syncthreads();
+    double2 hcn[H], own[H];
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+      hcn[t] = __ldg(hc + (long long)n * H + t);
+      own[t] = __ldg(ow + (long long)n * H + t);
+    }
+    double2 d[L];  // head values re-read per frequency (L1-resident, H*N doubles)
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      d[j] = cscale(hcn[0], j < Lk ? __ldg(g + i0 + j) : 0.0);
+#pragma unroll
+      for (int t = 1; t < H; ++t) d[j] = cfma(hcn[t], make_double2(j < Lk ? __ldg(g + (long long)t * N + i0 + j) : 0.0, 0.0), d[j]);
+    }
+    tri_solve_regs<NT>(d, cf, Lk, i0, R2POW, SPOW, tot, bc);
+#pragma unroll
+    for (int a = 0; a < H; ++a)
+#pragma unroll
+      for (int j = 0; j < L; ++j) acc[a][j] += own[a].x * d[j].x - own[a].y * d[j].y;
+  }
+#pragma unroll
+  for (int a = 0; a < H; ++a)
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (j < Lk) part[((long long)blockIdx.x * H + a) * N + i0 + j] = acc[a][j];
 }
 
 template <int NT>
@@ -163,7 +225,31 @@ cudaError_t launch_nt(double2* Sh, int nx, int nfreq, const pd_tri_coef* coef, c
   return cudaGetLastError();
 }
 
+template <int NT>
+cudaError_t launch_tail_nt(const double* g, double* part, int G, int N, int F, int H, const pd_tri_coef* coef,
+                           const double2* hc, const double2* ow, cudaStream_t st) {
+  if (H == 2)
+    tail1d_kernel<NT, 2><<<G, NT, 0, st>>>(g, part, N, F, coef, hc, ow);
+  else
+    tail1d_kernel<NT, 1><<<G, NT, 0, st>>>(g, part, N, F, coef, hc, ow);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t pd_launch_tail1d(const double* g, double* part, int G, int nx, int nfreq, int H, const pd_tri_coef* coef,
+                             const double2* hc, const double2* ow, cudaStream_t st) {
+  if (H < 1 || H > 2) return cudaErrorInvalidValue;
+  switch (pd_tridiag_threads(nx)) {
+    case 32: return launch_tail_nt<32>(g, part, G, nx, nfreq, H, coef, hc, ow, st);
+    case 64: return launch_tail_nt<64>(g, part, G, nx, nfreq, H, coef, hc, ow, st);
+    case 128: return launch_tail_nt<128>(g, part, G, nx, nfreq, H, coef, hc, ow, st);
+    case 256: return launch_tail_nt<256>(g, part, G, nx, nfreq, H, coef, hc, ow, st);
+    case 512: return launch_tail_nt<512>(g, part, G, nx, nfreq, H, coef, hc, ow, st);
+    case 1024: return launch_tail_nt<1024>(g, part, G, nx, nfreq, H, coef, hc, ow, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 int pd_tridiag_rows_per_thread() { return kL; }
 
