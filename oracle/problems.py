@@ -58,7 +58,7 @@ def K_matrix(cfg) -> sp.csr_matrix:
     if cfg.op == ADE2D:
         n = cfg.nx
         assert cfg.ny == n
-        h = 2.0 * math.pi / n
+        h = cfg.h  # domain length / N: [0, 2pi) for configs 3-4, (0, 1) for Table ctp-01 (P:l.908-912)
         lap, d1 = _periodic_1d(n, h)
         eye = sp.identity(n, format="csr")
         return (cfg.nu * (sp.kron(eye, lap) + sp.kron(lap, eye))

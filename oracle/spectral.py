@@ -56,7 +56,7 @@ def symbol_2d(cfg) -> np.ndarray:
     theta = 2 pi k / N.  (Pinned against the sparse stencil in tests/test_oracle_pins.py.)
     """
     n = cfg.nx
-    h = 2.0 * math.pi / n
+    h = cfg.h  # domain length / N
     th = 2.0 * math.pi * np.arange(n) / n
     sx = np.sin(th / 2) ** 2
     kap = (4.0 * cfg.nu / h ** 2) * (sx[None, :] + sx[:, None]) \

@@ -33,13 +33,19 @@ struct SlabCfg {
 #ifndef PD_SLAB_COLS_RM
 #define PD_SLAB_COLS_RM 8
 #endif
+#ifndef PD_SLAB_COLS_C
+#define PD_SLAB_COLS_C 8
+#endif
+#ifndef PD_SLAB_COLS_MINB
+#define PD_SLAB_COLS_MINB 2
+#endif
 template <int N>
 struct ColCfg {
-  static constexpr int C = kBatch;
+  static constexpr int C = PD_SLAB_COLS_C;  // columns per CTA (C * 16 B row segments)
   static constexpr int RM = PD_SLAB_COLS_RM;
   static constexpr int E = elems_per_thread(N, RM);
   static constexpr int NTH = C * N / E;
-  static constexpr int MINB = NTH <= 256 ? 2 : NTH <= 512 ? 2 : 1;
+  static constexpr int MINB = NTH <= 512 ? PD_SLAB_COLS_MINB : 1;
 };
 
 // rows [blockIdx.x*C, +C) of the flattened chunk (row index over slabs: slab*N + y), FFT along x in place
@@ -133,6 +139,10 @@ template <int N>
 int smem_bytes() {
   return smem_elems(kBatch * N) * (int)sizeof(double2);
 }
+template <int N>
+int smem_cols() {
+  return smem_elems(ColCfg<N>::C * N) * (int)sizeof(double2);
+}
 
 template <int N>
 cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2* lam2, const double* sx,
@@ -146,7 +156,7 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(slab_cols_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e = cudaFuncSetAttribute(slab_cols_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cols<N>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -156,7 +166,7 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
     double2* base = Sh + (long long)s0 * N * N;
     const unsigned row_ctas = (unsigned)(ns * (N / T::C));
     if (!cols_only) slab_rows_kernel<N, false><<<row_ctas, T::NTH, smem, st>>>(base, tw);
-    slab_cols_kernel<N><<<dim3(N / T::C, ns), ColCfg<N>::NTH, smem, st>>>(Sh, s0, lam1, lam2, sx, sn, prm, tw);
+    slab_cols_kernel<N><<<dim3(N / ColCfg<N>::C, ns), ColCfg<N>::NTH, smem_cols<N>(), st>>>(Sh, s0, lam1, lam2, sx, sn, prm, tw);
     if (!cols_only) slab_rows_kernel<N, true><<<row_ctas, T::NTH, smem, st>>>(base, tw);
     nl += cols_only ? 1 : 3;
   }
@@ -174,12 +184,12 @@ cudaError_t filter_n(double2* slab, const double2* tab, const double2* tw, cudaS
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(slab_cols_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e = cudaFuncSetAttribute(slab_cols_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cols<N>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   slab_rows_kernel<N, false><<<N / T::C, T::NTH, smem, st>>>(slab, tw);
-  slab_cols_kernel<N, true><<<dim3(N / T::C, 1), ColCfg<N>::NTH, smem, st>>>(slab, 0, nullptr, nullptr, nullptr,
+  slab_cols_kernel<N, true><<<dim3(N / ColCfg<N>::C, 1), ColCfg<N>::NTH, smem_cols<N>(), st>>>(slab, 0, nullptr, nullptr, nullptr,
                                                                            nullptr, pd_slab_params{}, tw, tab);
   slab_rows_kernel<N, true><<<N / T::C, T::NTH, smem, st>>>(slab, tw);
   return cudaGetLastError();

@@ -142,22 +142,34 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_inv_s1(const double2* __r
   }
   __syncthreads();
   // (0) rows n <= Nt/2 of the residue set -> A_n = E_n + i O_n and the mirror row A_{Nt-n}[-k]
+  // all of a thread's row loads are issued before any use (up to 2 N1 rows x 2 halves in flight)
   const int nsets = n2p == n2 ? 1 : 2;
-  const int total = nsets * N1 * NP;
-  for (int o = threadIdx.x; o < total; o += NTH) {
-    const int k = o & (NP - 1);
-    const int rowi = o / NP, set = rowi / N1, n1 = rowi % N1;
-    const int n = (set ? n2p : n2) + N2 * n1;
-    if (n > NT / 2) continue;
-    const double2* q = Sh + (long long)n * S + 2 * p0;
-    const double2 x0 = __ldcs(q + k), x1 = __ldcs(q + k + NP);
-    const double2 E = cadd(x0, x1);
-    const double2 O = cmulc(csub(x0, x1), s_twx[k]);  // (x0 - x1) w^-k
-    sm[pad((2 * n1 + set) * NP + k)] = make_double2(E.x - O.y, E.y + O.x);
-    if (n != 0 && n != NT / 2) {
-      const int m = NT - n;
-      const int setp = (m % N2) == n2 ? 0 : 1, n1p = m / N2;
-      sm[pad((2 * n1p + setp) * NP + ((NP - k) & (NP - 1)))] = make_double2(E.x + O.y, O.x - E.y);
+  for (int k = threadIdx.x; k < NP; k += NTH) {
+    double2 x0[2 * N1], x1[2 * N1];
+#pragma unroll
+    for (int r = 0; r < 2 * N1; ++r) {
+      const int set = r / N1, n1 = r % N1;
+      const int n = (set ? n2p : n2) + N2 * n1;
+      if (set < nsets && n <= NT / 2) {
+        const double2* q = Sh + (long long)n * S + 2 * p0 + k;
+        x0[r] = __ldcs(q);
+        x1[r] = __ldcs(q + NP);
+      }
+    }
+    const double2 wk = s_twx[k];
+#pragma unroll
+    for (int r = 0; r < 2 * N1; ++r) {
+      const int set = r / N1, n1 = r % N1;
+      const int n = (set ? n2p : n2) + N2 * n1;
+      if (!(set < nsets && n <= NT / 2)) continue;
+      const double2 E = cadd(x0[r], x1[r]);
+      const double2 O = cmulc(csub(x0[r], x1[r]), wk);  // (x0 - x1) w^-k
+      sm[pad((2 * n1 + set) * NP + k)] = make_double2(E.x - O.y, E.y + O.x);
+      if (n != 0 && n != NT / 2) {
+        const int m = NT - n;
+        const int setp = (m % N2) == n2 ? 0 : 1, n1p = m / N2;
+        sm[pad((2 * n1p + setp) * NP + ((NP - k) & (NP - 1)))] = make_double2(E.x + O.y, O.x - E.y);
+      }
     }
   }
   __syncthreads();

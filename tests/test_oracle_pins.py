@@ -130,9 +130,11 @@ def test_alpha_one_identity_column():
 
 
 # ----------------------------------------------------------------------------- spatial operator
-def test_symbol_2d_matches_stencil():
-    """kappa (reading c14) reproduces the sparse periodic stencil K on random data (ax != ay catches a transpose)."""
-    cfg = W.CONFIGS[3].scaled(nx=8, ny=8, nu=0.3, ax=1.0, ay=-0.4)
+@pytest.mark.parametrize("domain", [0.0, 1.0])
+def test_symbol_2d_matches_stencil(domain):
+    """kappa (reading c14) reproduces the sparse periodic stencil K on random data (ax != ay catches a transpose),
+    on [0, 2pi) (configs 3-4) and (0, 1) (Table ctp-01)."""
+    cfg = W.CONFIGS[3].scaled(nx=8, ny=8, nu=0.3, ax=1.0, ay=-0.4, domain=domain)
     n = cfg.nx
     u = np.random.default_rng(1).standard_normal(n * n)
     Ku = problems.K_matrix(cfg) @ u
@@ -140,6 +142,10 @@ def test_symbol_2d_matches_stencil():
     uh = Fn @ u.reshape(n, n) @ Fn.T
     Ku2 = (Fi @ (spectral.symbol_2d(cfg) * uh) @ Fi.T).real.reshape(-1) / n ** 2
     assert rel(Ku2, Ku) < 1e-13
+    # the centred stencil itself on the domain's spacing h = length / N
+    h = cfg.h
+    K = problems.K_matrix(cfg).toarray()
+    assert K[1, 0] == pytest.approx(-0.3 / h ** 2 - 1.0 / (2 * h)) and K[1, 1] == pytest.approx(4 * 0.3 / h ** 2)
 
 
 def test_1d_operators_stencil():

@@ -54,7 +54,8 @@ class Config:
     maxit: int = 100
     seed: int = 0
     source: str = "zero"         # "zero" | "sin8cos"
-    init: str = "sin_noise"      # "sin_noise" | "bump" | "fourier8" | "exact_wave"
+    init: str = "sin_noise"      # "sin_noise" | "bump" | "fourier8" | "exact_wave" | "gauss20"
+    domain: float = 0.0          # 2D domain length; 0 = the default [0, 2pi) (configs 3-4)
 
     @property
     def dt(self) -> float:
@@ -62,13 +63,15 @@ class Config:
 
     @property
     def length(self) -> float:
-        return 1.0 if self.op in (ADE1D, WAVE1D) else 2.0 * math.pi
+        if self.op in (ADE1D, WAVE1D):
+            return 1.0
+        return self.domain if self.domain > 0 else 2.0 * math.pi
 
     @property
     def h(self) -> float:
         if self.op in (ADE1D, WAVE1D):
             return 1.0 / (self.nx + 1)
-        return 2.0 * math.pi / self.nx
+        return self.length / self.nx
 
     @property
     def S(self) -> int:
@@ -99,13 +102,24 @@ CONFIGS = [
 ]
 BY_NAME = {c.name: c for c in CONFIGS}
 
+# Table ctp-01 (P:l.954-978): eq 2.14 on Omega = (0,1)^2 periodic, u_t - nu Lap u + grad u = 0
+# (advection (1, 1), reading x1), dx = dy = dt = 1/128, Nt = 512, alpha = 0.02, tol = 1e-6, stationary eq 2.10.
+CTP01_NUS = (1.0, 1e-1, 1e-2, 1e-3, 1e-4, 1e-5)
+CTP01_COUNTS = {BE: (4, 4, 5, 5, 5, 5), CN: (4, 5, 5, 5, 5, 5)}   # printed iteration numbers (B-E, TR)
+
+
+def ctp01_config(scheme: str, nu: float, **kw) -> Config:
+    c = Config("ctp01", ADE2D, nx=128, ny=128, nt=512, T=4.0, scheme=scheme, alpha=0.02, nu=nu, ax=1.0, ay=1.0,
+               solver="stationary", tol=1e-6, seed=0, init="gauss20", domain=1.0)
+    return c.scaled(**kw) if kw else c
+
 
 def grid(cfg: Config):
     """Node coordinates (reading c13). 1D: x[Nx]; 2D: (X, Y) each [N][N], x fastest."""
     if cfg.op in (ADE1D, WAVE1D):
         return (np.arange(cfg.nx, dtype=np.float64) + 1.0) * cfg.h
     x = np.arange(cfg.nx, dtype=np.float64) * cfg.h
-    y = np.arange(cfg.ny, dtype=np.float64) * (2.0 * math.pi / cfg.ny)
+    y = np.arange(cfg.ny, dtype=np.float64) * (cfg.length / cfg.ny)
     Y, X = np.meshgrid(y, x, indexing="ij")
     return X, Y
 
@@ -120,6 +134,9 @@ def initial_u0(cfg: Config) -> np.ndarray:
         x = grid(cfg)
         c = rng.uniform(0.3, 0.7)
         return np.exp(-((x - c) ** 2) / (2.0 * 0.05 ** 2))
+    if cfg.init == "gauss20":              # Table ctp-01 (P:l.910-912): exp(-20((x-1/2)^2 + (y-1/2)^2))
+        X, Y = grid(cfg)
+        return np.exp(-20.0 * ((X - 0.5) ** 2 + (Y - 0.5) ** 2)).reshape(-1)
     if cfg.init == "fourier8":             # configs 3, 4 (reading c12)
         X, Y = grid(cfg)
         u = np.zeros_like(X)
