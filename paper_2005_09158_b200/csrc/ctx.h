@@ -74,6 +74,8 @@ struct pd_ctx {
   double* sx = nullptr;          // 2D: sin^2(pi k / N)
   double* sn = nullptr;          // 2D: sin(2 pi k / N)
   double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
+  pd_ytri_coef* ytri = nullptr;  // 2D: [F][N] cyclic Toeplitz y-pass constants (slab2d.cu ytri)
+  bool use_ytri = false;
   pd_slab_params slab{};
   int slab_chunk = 1;
   pd_stencil sten{};

@@ -67,6 +67,19 @@ struct pd_slab_params {
   double cx, cy; // ax / h, ay / h
 };
 int pd_slab2d_supported(int n);
+// Step (b) 2D, y-direction as cyclic Toeplitz tridiagonal solves on x-transformed slabs (slab2d.cu ytri):
+// per (frequency n, kx): a x_{y-1} + b x_y + c x_{y+1} = d_y (periodic in y), a = lam2 k2y_m, c = lam2 k2y_p,
+// b = lam1 + lam2 (kappa_x(kx) + 2 nu/h^2).  Roots of c r^2 + b r + a: r = a tau (|r| <= 1), s = c tau (|s| <= 1),
+// tau = 2/(-b -+ sqrt(b^2 - 4ac)) (larger denominator):  w_y = r w_{y-1} + d_y,  x_y = s x_{y+1} - tau w_y, with
+// the cyclic closures w_{N-1} = w'_{N-1}/(1 - r^N), x_0 = x'_0/(1 - s^N).  One table entry per (n, kx).
+struct pd_ytri_coef {
+  double2 r, s, tau;
+  double2 ir;   // 1 / (1 - r^N)
+  double2 is;   // 1 / (1 - s^N)
+  double2 rL;   // r^L, L = N/32 rows per lane
+  double2 sL;   // s^L
+};
+int pd_slab2d_ytri_supported(int n);
 int pd_slab2d_chunk(int n, int nfreq);
 // chunk = slabs per L2-resident chunk; *launches = kernels launched
 // one N x N complex slab in place: 2D FFT, multiply by tab[ky*N + kx] / N^2, inverse 2D FFT (tail map, tail.cu)
@@ -74,6 +87,10 @@ cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, co
 cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                              const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
                              int chunk, int cols_only, cudaStream_t st, int* launches);
+// the y-pass of Step (b) by cyclic Toeplitz solves (x already transformed, by tfx.cu or by the slab row pass when
+// rows != 0): frequencies [f0_glob, f0_glob + nfreq) of coef ([F_all][N]); scale applied to the result
+cudaError_t pd_launch_slab2d_ytri(double2* Sh, int n, int nfreq, int f0_glob, const pd_ytri_coef* coef, double scale,
+                                  const double2* tw, int chunk, int rows, cudaStream_t st, int* launches);
 
 // ---- all-at-once residual / matvec (stencil.cu) ----
 struct pd_stencil {

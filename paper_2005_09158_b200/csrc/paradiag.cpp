@@ -72,6 +72,50 @@ static void closed_form_spectra(int nt, double alpha, double dt, pd_scheme s, st
 
 static inline double2 d2(cld v) { return make_double2((double)v.real(), (double)v.imag()); }
 
+// 2D y-pass as cyclic Toeplitz solves (slab2d.cu ytri): per (n, kx) constants; false when any column falls
+// outside the stable regime (|r| or |s| > 1, or a closure denominator 1 - r^N near 0): the FFT column pass is
+// used instead.
+static bool ytri_coefs(const pd_ctx* c, const std::vector<cld>& l1, const std::vector<cld>& l2,
+                       std::vector<pd_ytri_coef>& out) {
+  const int N = c->g.nx, L = N / 32;
+  const long double h = (long double)c->g.length / N, nu = c->g.nu;
+  const long double km = -nu / (h * h) - (long double)c->g.ay / (2 * h), kp = -nu / (h * h) + (long double)c->g.ay / (2 * h);
+  const long double kd = 4 * nu / (h * h), cx = (long double)c->g.ax / h;
+  out.resize((size_t)c->F * N);
+  auto cp = [](cld m, int e) {
+    cld r = 1.0L;
+    while (e) {
+      if (e & 1) r *= m;
+      m *= m;
+      e >>= 1;
+    }
+    return r;
+  };
+  for (int n = 0; n < c->F; ++n)
+    for (int kx = 0; kx < N; ++kx) {
+      const long double pi = 3.141592653589793238462643383279502884L, sk = sinl(pi * kx / N);
+      const cld kapx(kd * sk * sk, cx * sinl(2.0L * pi * kx / N));
+      const cld A = l2[n] * km, Cc = l2[n] * kp, B = l1[n] + l2[n] * (kapx + 2 * nu / (h * h));
+      const cld D = std::sqrt(B * B - 4.0L * A * Cc);
+      const cld den1 = -B - D, den2 = -B + D;
+      const cld den = std::abs(den1) >= std::abs(den2) ? den1 : den2;
+      if (std::abs(den) == 0.0L) return false;
+      const cld tau = 2.0L / den, r = A * tau, sv = Cc * tau;
+      if (!(std::abs(r) <= 1.0L) || !(std::abs(sv) <= 1.0L)) return false;
+      const cld rN = cp(r, N), sN = cp(sv, N);
+      if (std::abs(1.0L - rN) < 1e-6L || std::abs(1.0L - sN) < 1e-6L) return false;
+      pd_ytri_coef& t = out[(size_t)n * N + kx];
+      t.r = d2(r);
+      t.s = d2(sv);
+      t.tau = d2(tau);
+      t.ir = d2(1.0L / (1.0L - rN));
+      t.is = d2(1.0L / (1.0L - sN));
+      t.rL = d2(cp(r, L));
+      t.sL = d2(cp(sv, L));
+    }
+  return true;
+}
+
 // per-frequency constants of the Toeplitz tridiagonal recurrence solver (tridiag.cu)
 static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vector<cld>& l2, double sub, double dia,
                            double sup, std::vector<pd_tri_coef>& out) {
@@ -124,6 +168,7 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
 static void free_ctx(pd_ctx* c) {
   if (!c) return;
   pd_tail_free(c);
+  if (c->ytri) cudaFree(c->ytri);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
   for (void* p : ptrs)
@@ -328,6 +373,15 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     SETUP_CUDA(cudaMemcpy(c->sn, hsn.data(), N * sizeof(double), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->tw_s, htws.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
     c->slab_chunk = pd_slab2d_chunk(N, c->F);
+    // y-pass by cyclic Toeplitz solves where every column is in the stable regime (PD_NO_YTRI: FFT column pass)
+    if (pd_slab2d_ytri_supported(N) && getenv("PD_NO_YTRI") == nullptr) {
+      std::vector<pd_ytri_coef> yt;
+      if (ytri_coefs(c, l1, l2, yt)) {
+        SETUP_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->ytri), yt.size() * sizeof(pd_ytri_coef)));
+        SETUP_CUDA(cudaMemcpy(c->ytri, yt.data(), yt.size() * sizeof(pd_ytri_coef), cudaMemcpyHostToDevice));
+        c->use_ytri = true;
+      }
+    }
     if (const char* e = getenv("PD_SLAB_CHUNK_MB")) {
       const long long sb = (long long)N * N * 16;
       c->slab_chunk = (int)std::max(1LL, std::min<long long>(c->F, (atoll(e) << 20) / sb));
@@ -480,8 +534,12 @@ pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   phase_begin(c, 1);
   if (c->g.op == PD_ADE2D_PERIODIC) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
-                                c->slab_chunk, c->use_tfx ? 1 : 0, c->st, &nl));
+    if (c->use_ytri)
+      PD_CUDA(c, pd_launch_slab2d_ytri(Sh, c->g.nx, nfreq, f0, c->ytri, 1.0 / c->g.nx, c->tw_s, c->slab_chunk,
+                                       c->use_tfx ? 0 : 1, c->st, &nl));
+    else
+      PD_CUDA(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
+                                  c->slab_chunk, c->use_tfx ? 1 : 0, c->st, &nl));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tridiag(Sh, c->g.nx, nfreq, c->tri + f0, pd_tridiag_rows_per_thread(), c->st));

@@ -174,6 +174,151 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// y-pass by cyclic Toeplitz tridiagonal solves (see kernels.h pd_ytri_coef).  8 columns per CTA, one warp per
+// column, L = N/32 consecutive rows per lane in registers; first-order recurrences carried across lanes by warp
+// affine scans, cyclic closures from the scan totals.  ~26 fp64 operations per complex element instead of the
+// ~150 of FFT -> divide -> IFFT, so the pass is HBM-bound.  smem: padded column-major tile
+// (index c*(N+33) + i + i/L) - conflict-free both for the coalesced row loads and for the lane chunks.
+PD_D double2 shfl_up2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+PD_D double2 shfl_down2(double2 v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+PD_D double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+PD_D double2 cpow_small(double2 m, int e) {
+  double2 r = make_double2(1.0, 0.0);
+  while (e) {
+    if (e & 1) r = cmul(r, m);
+    m = cmul(m, m);
+    e >>= 1;
+  }
+  return r;
+}
+// exclusive affine scan over the 32 lanes: I_l = M I_{l-1} + e_l; returns I_{l-1} (0 for the first lane);
+// *inc_last = the inclusive value at the last lane of the scan order (lane 31 forward, lane 0 reverse)
+template <bool REVERSE>
+PD_D double2 warp_affine_scan(double2 e, double2 M, double2* inc_last) {
+  const int lane = threadIdx.x & 31;
+  const int vl = REVERSE ? 31 - lane : lane;
+  double2 I = e, Md = M;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double2 o = REVERSE ? shfl_down2(I, d) : shfl_up2(I, d);
+    if (vl >= d) I = cfma(Md, o, I);
+    Md = cmul(Md, Md);
+  }
+  *inc_last = shfl2(I, REVERSE ? 0 : 31);
+  const double2 ex = REVERSE ? shfl_down2(I, 1) : shfl_up2(I, 1);
+  return vl == 0 ? czero() : ex;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, N <= 256 ? 3 : N <= 512 ? 2 : 1) slab_ytri_kernel(double2* __restrict__ Sh, int slab0,
+                                                                          int fglob0,
+                                                                          const pd_ytri_coef* __restrict__ coef,
+                                                                          double scale) {
+  constexpr int L = N / 32, CS = N + 33;
+  extern __shared__ double2 sm[];
+  const int n = slab0 + blockIdx.y;
+  const int c0 = blockIdx.x * 8;
+  double2* slab = Sh + (long long)n * N * N + c0;
+  {
+    // all N*8/256 loads of a thread in flight before the first smem store
+    constexpr int PT = N * 8 / 256;
+    double2 v[PT];
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int i = threadIdx.x + k * 256, r = i >> 3, c = i & 7;
+      v[k] = __ldcs(slab + (long long)r * N + c);
+    }
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int i = threadIdx.x + k * 256, r = i >> 3, c = i & 7;
+      sm[c * CS + r + r / L] = v[k];
+    }
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const pd_ytri_coef cf = coef[(long long)(fglob0 + blockIdx.y) * N + c0 + w];
+  double2* col = sm + w * CS + lane * (L + 1);  // rows lane*L .. lane*L + L - 1 (+ one pad per lane chunk)
+  double2 d[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) d[j] = col[j];
+  // forward: w'_i = r w'_{i-1} + d_i (zero carry-in), lane carries by scan, closure W = w_{N-1}
+  double2 p = czero();
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    p = cfma(cf.r, p, d[j]);
+    d[j] = p;
+  }
+  double2 tot;
+  const double2 cin = warp_affine_scan<false>(p, cf.rL, &tot);
+  const double2 W = cmul(tot, cf.ir);
+  double2 q = cfma(cpow_small(cf.rL, lane), W, cin);  // carry + r^{lane L} W
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    q = cmul(cf.r, q);
+    d[j] = cadd(d[j], q);
+  }
+  // backward: x'_i = s x'_{i+1} - tau w_i (zero carry-in from the right), scan from the last lane, closure x_0
+  const double2 mtau = cneg(cf.tau);
+  p = czero();
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j) {
+    p = cfma(cf.s, p, cmul(mtau, d[j]));
+    d[j] = p;
+  }
+  const double2 cr = warp_affine_scan<true>(p, cf.sL, &tot);
+  const double2 x0 = cmul(tot, cf.is);
+  q = cfma(cpow_small(cf.sL, 31 - lane), x0, cr);  // carry + s^{N - lane L - L} x_0
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j) {
+    q = cmul(cf.s, q);
+    d[j] = cscale(cadd(d[j], q), scale);
+  }
+#pragma unroll
+  for (int j = 0; j < L; ++j) col[j] = d[j];
+  __syncthreads();
+#pragma unroll 8
+  for (int i = threadIdx.x; i < N * 8; i += 256) {
+    const int r = i >> 3, c = i & 7;
+    __stcs(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
+  }
+}
+
+template <int N>
+cudaError_t ytri_n(double2* Sh, int nfreq, int f0g, const pd_ytri_coef* coef, double scale, const double2* tw,
+                   int chunk, int rows, cudaStream_t st, int* launches) {
+  using T = SlabCfg<N>;
+  const int smem = 8 * (N + 33) * (int)sizeof(double2), smr = smem_bytes<N>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(slab_ytri_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(slab_rows_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int nl = 0;
+  for (int s0 = 0; s0 < nfreq; s0 += chunk) {
+    const int ns = nfreq - s0 < chunk ? nfreq - s0 : chunk;
+    double2* base = Sh + (long long)s0 * N * N;
+    const unsigned row_ctas = (unsigned)(ns * (N / T::C));
+    if (rows) slab_rows_kernel<N, false><<<row_ctas, T::NTH, smr, st>>>(base, tw);
+    slab_ytri_kernel<N><<<dim3(N / 8, ns), 256, smem, st>>>(Sh, s0, f0g + s0, coef, scale);
+    if (rows) slab_rows_kernel<N, true><<<row_ctas, T::NTH, smr, st>>>(base, tw);
+    nl += rows ? 3 : 1;
+  }
+  if (launches) *launches = nl;
+  return cudaGetLastError();
+}
+
 template <int N>
 cudaError_t filter_n(double2* slab, const double2* tab, const double2* tw, cudaStream_t st) {
   using T = SlabCfg<N>;
@@ -206,6 +351,21 @@ cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, co
     case 256: return filter_n<256>(slab, tab, tw, st);
     case 512: return filter_n<512>(slab, tab, tw, st);
     case 1024: return filter_n<1024>(slab, tab, tw, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int pd_slab2d_ytri_supported(int n) { return n == 32 || n == 64 || n == 128 || n == 256 || n == 512 || n == 1024; }
+
+cudaError_t pd_launch_slab2d_ytri(double2* Sh, int n, int nfreq, int f0_glob, const pd_ytri_coef* coef, double scale,
+                                  const double2* tw, int chunk, int rows, cudaStream_t st, int* launches) {
+  switch (n) {
+    case 32: return ytri_n<32>(Sh, nfreq, f0_glob, coef, scale, tw, chunk, rows, st, launches);
+    case 64: return ytri_n<64>(Sh, nfreq, f0_glob, coef, scale, tw, chunk, rows, st, launches);
+    case 128: return ytri_n<128>(Sh, nfreq, f0_glob, coef, scale, tw, chunk, rows, st, launches);
+    case 256: return ytri_n<256>(Sh, nfreq, f0_glob, coef, scale, tw, chunk, rows, st, launches);
+    case 512: return ytri_n<512>(Sh, nfreq, f0_glob, coef, scale, tw, chunk, rows, st, launches);
+    case 1024: return ytri_n<1024>(Sh, nfreq, f0_glob, coef, scale, tw, chunk, rows, st, launches);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -113,10 +113,21 @@ tfft_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long lon
   // stage the half-spectrum tile H[n][col], n = 0..N/2, col = 0..2C-1 (coalesced rows)
   constexpr int NIN = (N / 2 + 1) * 2 * C;
   const double2* in = Sh + s0;
-#pragma unroll 4
-  for (int o = threadIdx.x; o < NIN; o += NTH) {
-    const int col = o % (2 * C), n = o / (2 * C);
-    sm[pad(o)] = (full || s0 + col < S) ? __ldcs(in + (long long)n * S + col) : czero();
+  {
+    // all of a thread's loads in flight before the first smem store
+    constexpr int PT = (NIN + NTH - 1) / NTH;
+    double2 v[PT];
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int o = threadIdx.x + k * NTH;
+      const int col = o % (2 * C), n = o / (2 * C);
+      v[k] = (o < NIN && (full || s0 + col < S)) ? __ldcs(in + (long long)n * S + col) : czero();
+    }
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int o = threadIdx.x + k * NTH;
+      if (o < NIN) sm[pad(o)] = v[k];
+    }
   }
   __syncthreads();
   const double invN = 1.0 / N;

@@ -120,15 +120,26 @@ tf4_inv_s1(const double2* __restrict__ Sh, long long S, long long p_begin, long 
   // stage the half-spectrum rows n <= Nt/2 with n % N2 in {n2, n2'}: slot (set, n1) -> 2P complex
   const int nsets = (n2p == n2) ? 1 : 2;
   const int total = nsets * N1 * 2 * kP;
-  for (int o = threadIdx.x; o < total; o += NTH) {
-    const int col = o % (2 * kP);
-    const int rowi = o / (2 * kP);
-    const int set = rowi / N1, n1 = rowi % N1;
-    const int n = (set == 0 ? n2 : n2p) + kN2 * n1;
-    const long long gcol = 2 * p0 + col;
-    double2 v = czero();
-    if (n <= NT / 2 && pl0 + (col >> 1) < Pc && gcol < S) v = __ldcs(Sh + (long long)n * S + gcol);
-    sm[pad(o)] = v;
+  {
+    // all of a thread's loads in flight before the first smem store
+    constexpr int PT = (2 * N1 * 2 * kP + NTH - 1) / NTH;
+    double2 v[PT];
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int o = threadIdx.x + k * NTH;
+      const int col = o % (2 * kP);
+      const int rowi = o / (2 * kP);
+      const int set = rowi / N1, n1 = rowi % N1;
+      const int n = (set == 0 ? n2 : n2p) + kN2 * n1;
+      const long long gcol = 2 * p0 + col;
+      v[k] = czero();
+      if (o < total && n <= NT / 2 && pl0 + (col >> 1) < Pc && gcol < S) v[k] = __ldcs(Sh + (long long)n * S + gcol);
+    }
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int o = threadIdx.x + k * NTH;
+      if (o < total) sm[pad(o)] = v[k];
+    }
   }
   __syncthreads();
   const bool fullp = pl0 + kP <= Pc;

@@ -144,8 +144,20 @@ __global__ void __launch_bounds__(NT) tridiag_kernel(double2* __restrict__ Sh, i
   const pd_tri_coef cf = coef[n];
   double2* row = Sh + (long long)n * N;
   tri_tables(cf, R2POW, SPOW);
-  // coalesced load into padded staging: element i -> i + i/L
-  for (int i = threadIdx.x; i < N; i += NT) sbuf[i + i / L] = __ldcs(row + i);
+  // coalesced load into padded staging: element i -> i + i/L (all of a thread's loads in flight first)
+  {
+    double2 v[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const int i = threadIdx.x + k * NT;
+      if (i < N) v[k] = __ldcs(row + i);
+    }
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const int i = threadIdx.x + k * NT;
+      if (i < N) sbuf[i + i / L] = v[k];
+    }
+  }
   __syncthreads();
 
   const int k = threadIdx.x;

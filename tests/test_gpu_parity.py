@@ -237,3 +237,14 @@ def test_spectra_match_oracle():
         l1, l2 = make_ctx(cfg.scaled(nx=min(cfg.nx, 64), ny=min(cfg.ny, 64))).spectra()
         o1, o2 = spectral.spectra(cfg)
         assert rel(l1, o1) < 1e-13 and rel(l2, o2) < 1e-13
+
+
+@pytest.mark.parametrize("nx,nt", [(64, 16), (128, 1024), (32, 2048)])
+def test_apply_2d_fft_column_pass_matches_oracle(nx, nt, monkeypatch):
+    """The FFT column pass (divide by lambda1 + lambda2 kappa) is kept as the fallback of the cyclic Toeplitz
+    y-pass (PD_NO_YTRI, or any column outside the stable regime): same parity bar."""
+    monkeypatch.setenv("PD_NO_YTRI", "1")
+    cfg = _cfg(W.ADE2D, W.CN, nx, nt, alpha=0.02)
+    r = W.random_vector(cfg, seed=nx + nt)
+    z = to_host(make_ctx(cfg).apply_precond(to_dev(r)))
+    check_apply(cfg, r, z)
