@@ -18,7 +18,7 @@ import math
 import numpy as np
 
 from . import problems
-from workloads import ADE1D, ADE2D, BE, CN, LF, WAVE1D
+from workloads import ADE1D, ADE2D, BE, CN, LF, WAVE1D, WAVE2D
 
 
 def _matpow(G: np.ndarray, n: int) -> np.ndarray:
@@ -114,8 +114,16 @@ def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
         mu = symbol_2d(cfg).reshape(-1)
         rh = (Fn @ r.reshape(nt, n, n) @ Fn.T).reshape(nt, n * n)
         to_nodal = lambda zh: ((Fi @ zh.reshape(nt, n, n) @ Fi.T) / (n * n)).real.reshape(nt, n * n)
+    elif cfg.op == WAVE2D:  # tensor DST-I basis, mu_{kl} = mu_k + mu_l
+        n, h = cfg.nx, cfg.h
+        j = np.arange(1, n + 1)
+        Q = math.sqrt(2.0 / (n + 1)) * np.sin(math.pi * np.outer(j, j) / (n + 1))
+        m1 = (4.0 / h ** 2) * np.sin(math.pi * j / (2 * (n + 1))) ** 2
+        mu = (m1[:, None] + m1[None, :]).reshape(-1)
+        rh = (Q @ r.reshape(nt, n, n) @ Q).reshape(nt, n * n)
+        to_nodal = lambda zh: (Q @ zh.reshape(nt, n, n) @ Q).reshape(nt, n * n)
     else:
-        raise ValueError("modal O2 needs a known eigenbasis (WAVE1D or ADE2D)")
+        raise ValueError("modal O2 needs a known eigenbasis (WAVE1D, ADE2D or WAVE2D)")
 
     if cfg.scheme in (BE, CN):
         th = problems.theta_of(cfg.scheme)

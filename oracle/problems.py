@@ -13,7 +13,7 @@ import math
 import numpy as np
 import scipy.sparse as sp
 
-from workloads import ADE1D, ADE2D, BE, CN, LF, WAVE1D
+from workloads import ADE1D, ADE2D, BE, CN, LF, WAVE1D, WAVE2D
 
 
 def theta_of(scheme: str) -> float:
@@ -43,6 +43,7 @@ def K_matrix(cfg) -> sp.csr_matrix:
     WAVE1D: K = A = -D2 (negative Laplacian, P:l.1208-1211)
     ADE2D : K = -nu Lap_h + ax Dx + ay Dy, 5-point Laplacian, periodic (P:l.908-918, reading c14);
             unknown index s = y*N + x (x fastest).
+    WAVE2D: K = -Lap_h, 5-point, homogeneous Dirichlet on (0,1)^2, interior nodes (Table T4A, P:l.1309-1313).
     """
     if cfg.op in (ADE1D, WAVE1D):
         n, h = cfg.nx, cfg.h
@@ -63,6 +64,13 @@ def K_matrix(cfg) -> sp.csr_matrix:
         eye = sp.identity(n, format="csr")
         return (cfg.nu * (sp.kron(eye, lap) + sp.kron(lap, eye))
                 + cfg.ax * sp.kron(eye, d1) + cfg.ay * sp.kron(d1, eye)).tocsr()
+    if cfg.op == WAVE2D:
+        n, h = cfg.nx, cfg.h
+        assert cfg.ny == n
+        e = np.ones(n)
+        d2 = sp.diags([-e[:-1], 2.0 * e, -e[:-1]], [-1, 0, 1], shape=(n, n), format="csr") / h ** 2
+        eye = sp.identity(n, format="csr")
+        return (sp.kron(eye, d2) + sp.kron(d2, eye)).tocsr()
     raise ValueError(cfg.op)
 
 

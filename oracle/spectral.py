@@ -18,7 +18,7 @@ import numpy as np
 import scipy.linalg
 
 from . import problems
-from workloads import ADE1D, ADE2D, WAVE1D
+from workloads import ADE1D, ADE2D, WAVE1D, WAVE2D
 
 
 def gamma(nt: int, alpha: float) -> np.ndarray:
@@ -82,6 +82,8 @@ def step_b(cfg, S1: np.ndarray, lam1: np.ndarray, lam2: np.ndarray) -> np.ndarra
     1D (ADE1D, WAVE1D): pivoted banded LU (LAPACK gbsv via scipy.linalg.solve_banded) per n.
     2D periodic: K is diagonalised by the 2D DFT, so the solve is naive 2D DFT -> divide by
     lambda_1 + lambda_2 kappa(k) -> naive inverse 2D DFT (exact, not an approximation).
+    2D Dirichlet (WAVE2D): sparse direct LU of lambda_1 I + lambda_2 K per n (as the paper's Matlab code,
+    "MATLAB's sparse direct solver", P:l.1315-1316).
     """
     nt = S1.shape[0]
     S2 = np.empty_like(S1, dtype=np.complex128)
@@ -104,6 +106,14 @@ def step_b(cfg, S1: np.ndarray, lam1: np.ndarray, lam2: np.ndarray) -> np.ndarra
         Xh = Xh / (lam1[:, None, None] + lam2[:, None, None] * kap[None, :, :])
         Y = (Fi @ Xh @ Fi.T) / (n * n)
         return Y.reshape(nt, n * n)
+    if cfg.op == WAVE2D:
+        import scipy.sparse as sps
+        import scipy.sparse.linalg as spla
+        K = problems.K_matrix(cfg).astype(np.complex128)
+        eye = sps.identity(cfg.S, format="csc", dtype=np.complex128)
+        for k in range(nt):
+            S2[k] = spla.splu(sps.csc_matrix(lam1[k] * eye + lam2[k] * K)).solve(S1[k])
+        return S2
     raise ValueError(cfg.op)
 
 

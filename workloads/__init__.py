@@ -29,6 +29,7 @@ import numpy as np
 ADE1D = "ade1d"      # u_t = nu u_xx - a u_x on (0,1), homogeneous Dirichlet
 WAVE1D = "wave1d"    # u_tt = u_xx on (0,1), homogeneous Dirichlet
 ADE2D = "ade2d"      # u_t = nu Lap u - a.grad u on [0,2pi)^2, periodic
+WAVE2D = "wave2d"    # u_tt = Lap u + f on (0,1)^2, homogeneous Dirichlet (Table T4A, P:l.1309-1349)
 
 # scheme ids (mirror pd_scheme)
 BE, CN, LF = "be", "cn", "lf"
@@ -63,13 +64,13 @@ class Config:
 
     @property
     def length(self) -> float:
-        if self.op in (ADE1D, WAVE1D):
+        if self.op in (ADE1D, WAVE1D, WAVE2D):
             return 1.0
         return self.domain if self.domain > 0 else 2.0 * math.pi
 
     @property
     def h(self) -> float:
-        if self.op in (ADE1D, WAVE1D):
+        if self.op in (ADE1D, WAVE1D, WAVE2D):
             return 1.0 / (self.nx + 1)
         return self.length / self.nx
 
@@ -118,6 +119,10 @@ def grid(cfg: Config):
     """Node coordinates (reading c13). 1D: x[Nx]; 2D: (X, Y) each [N][N], x fastest."""
     if cfg.op in (ADE1D, WAVE1D):
         return (np.arange(cfg.nx, dtype=np.float64) + 1.0) * cfg.h
+    if cfg.op == WAVE2D:  # interior nodes of (0,1)^2
+        x = (np.arange(cfg.nx, dtype=np.float64) + 1.0) * cfg.h
+        Y, X = np.meshgrid(x[: cfg.ny], x, indexing="ij")
+        return X, Y
     x = np.arange(cfg.nx, dtype=np.float64) * cfg.h
     y = np.arange(cfg.ny, dtype=np.float64) * (cfg.length / cfg.ny)
     Y, X = np.meshgrid(y, x, indexing="ij")
@@ -134,6 +139,9 @@ def initial_u0(cfg: Config) -> np.ndarray:
         x = grid(cfg)
         c = rng.uniform(0.3, 0.7)
         return np.exp(-((x - c) ** 2) / (2.0 * 0.05 ** 2))
+    if cfg.init == "exact_wave2d":         # Table T4A: u0 = sin(pi x) sin(pi y) (P:l.1311-1313)
+        X, Y = grid(cfg)
+        return (np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1)
     if cfg.init == "gauss20":              # Table ctp-01 (P:l.910-912): exp(-20((x-1/2)^2 + (y-1/2)^2))
         X, Y = grid(cfg)
         return np.exp(-20.0 * ((X - 0.5) ** 2 + (Y - 0.5) ** 2)).reshape(-1)
@@ -159,6 +167,9 @@ def initial_v0(cfg: Config) -> np.ndarray:
     """u_t(0) for the wave problems ([S]); zeros elsewhere."""
     if cfg.init == "exact_wave":
         return np.sin(math.pi * grid(cfg))
+    if cfg.init == "exact_wave2d":         # u_1 = u_t(0) = sin(pi x) sin(pi y)
+        X, Y = grid(cfg)
+        return (np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1)
     return np.zeros(cfg.S)
 
 
@@ -173,6 +184,9 @@ def source_samples(cfg: Config):
         x = grid(cfg)
         shape = sum(a[k - 1] * np.sin(k * math.pi * x) for k in range(1, 9))
         return np.cos(t)[:, None] * shape[None, :]
+    if cfg.source == "exact_wave2d":       # f = (1 + 2 pi^2) sin(pi x) sin(pi y) e^t (P:l.1311-1313)
+        X, Y = grid(cfg)
+        return np.exp(t)[:, None] * ((1.0 + 2.0 * math.pi ** 2) * np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1)[None, :]
     if cfg.source == "exact_wave":         # f = (1 + pi^2) sin(pi x) e^t for u = sin(pi x) e^t
         x = grid(cfg)
         return np.exp(t)[:, None] * ((1.0 + math.pi ** 2) * np.sin(math.pi * x))[None, :]
@@ -188,7 +202,25 @@ def random_vector(cfg: Config, seed: int | None = None) -> np.ndarray:
 
 
 def exact_wave_solution(cfg: Config) -> np.ndarray:
-    """sin(pi x) e^{t_n}, n = 1..Nt ([Nt][S]) for the second-order pin of reading c4."""
-    x = grid(cfg)
+    """sin(pi x) e^{t_n} (1D) / sin(pi x) sin(pi y) e^{t_n} (2D, Table T4A), n = 1..Nt ([Nt][S])."""
     t = np.arange(1, cfg.nt + 1, dtype=np.float64) * cfg.dt
+    if cfg.op == WAVE2D:
+        X, Y = grid(cfg)
+        return np.exp(t)[:, None] * (np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1)[None, :]
+    x = grid(cfg)
     return np.exp(t)[:, None] * np.sin(math.pi * x)[None, :]
+
+
+# Table T4A (P:l.1309-1349, SURVEY 8(f) NEXT-3): u_tt = Lap u + f on (0,1)^2, T = 2, exact u = sin(pi x) sin(pi y) e^t,
+# implicit leapfrog (eq 3.2b), GMRES, zero initial guess, tol 1e-10.  Mesh label (Nx, Nx, Nt) read as h = 1/Nx
+# (Nx - 1 interior nodes per direction) and Nt - 1 time steps (the label counts the time points incl. t = 0;
+# reading x3, pinned by the printed errors).
+T4A_LABELS = (32, 64, 128, 256)
+T4A_ERRORS = (7.17e-3, 1.86e-3, 4.74e-4, 1.20e-4)          # alpha = 1 and alpha = 0.1 columns
+T4A_ITERS = {0.1: (3, 3, 3, 3), 1.0: (3, 7, 37, None)}      # None: "> 50"
+
+
+def t4a_config(label: int, alpha: float = 0.1, **kw) -> Config:
+    c = Config(f"t4a_{label}", WAVE2D, nx=label - 1, ny=label - 1, nt=label, T=2.0, scheme=LF, alpha=alpha,
+               nu=1.0, solver="gmres", tol=1e-10, m=50, maxit=50, seed=0, source="exact_wave2d", init="exact_wave2d")
+    return c.scaled(**kw) if kw else c
