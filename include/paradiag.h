@@ -54,12 +54,15 @@ typedef enum { PD_BE = 0, PD_CN = 1, PD_LEAPFROG = 2 } pd_scheme;
 typedef enum {
   PD_ADE1D_DIRICHLET = 0,  /* u_t = nu u_xx - ax u_x on (0,L), u=0 at both ends, Nx interior nodes, h = L/(Nx+1) */
   PD_WAVE1D_DIRICHLET = 1, /* u_tt = nu u_xx on (0,L), Dirichlet (nu = c^2; use PD_LEAPFROG)                  */
-  PD_ADE2D_PERIODIC = 2    /* u_t = nu Lap u - (ax, ay).grad u on [0,L)^2 periodic, N x N, h = L/N (5-point)  */
+  PD_ADE2D_PERIODIC = 2,   /* u_t = nu Lap u - (ax, ay).grad u on [0,L)^2 periodic, N x N, h = L/N (5-point)  */
+  PD_WAVE2D_DIRICHLET = 3  /* u_tt = nu Lap u on (0,L)^2, u = 0 on the boundary, N x N interior nodes,
+                              h = L/(N+1), N + 1 a power of two in [16, 512]; ax = ay = 0 (Table T4A,
+                              P:l.1309-1349; use PD_LEAPFROG).  Step (b) by the tensor DST-I (exact). */
 } pd_operator;
 
 typedef struct {
   pd_operator op;
-  int nx, ny;       /* 1D: nx = Nx, ny = 1.  2D: nx = ny = N (power of two) */
+  int nx, ny;       /* 1D: nx = Nx, ny = 1.  2D: nx = ny = N (periodic: power of two; Dirichlet: 2^k - 1) */
   double length;    /* domain length L (1 for the 1D configs, 2*pi for the 2D configs) */
   double nu, ax, ay;
 } pd_grid;

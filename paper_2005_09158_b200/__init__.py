@@ -12,6 +12,7 @@ from ._lib import (  # noqa: F401
     CN,
     LEAPFROG,
     WAVE1D_DIRICHLET,
+    WAVE2D_DIRICHLET,
     ParaDiag,
     ParaDiagError,
     Report,
@@ -22,4 +23,4 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = ["ParaDiag", "ParaDiagError", "Report", "load_library", "exported_symbols", "nccl_unique_id", "partition",
-           "ADE1D_DIRICHLET", "WAVE1D_DIRICHLET", "ADE2D_PERIODIC", "BE", "CN", "LEAPFROG"]
+           "ADE1D_DIRICHLET", "WAVE1D_DIRICHLET", "ADE2D_PERIODIC", "WAVE2D_DIRICHLET", "BE", "CN", "LEAPFROG"]

@@ -10,7 +10,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libparadiag.so")
 _HEADER = os.path.join(os.path.dirname(_HERE), "include", "paradiag.h")
 
-ADE1D_DIRICHLET, WAVE1D_DIRICHLET, ADE2D_PERIODIC = 0, 1, 2
+ADE1D_DIRICHLET, WAVE1D_DIRICHLET, ADE2D_PERIODIC, WAVE2D_DIRICHLET = 0, 1, 2, 3
 BE, CN, LEAPFROG = 0, 1, 2
 PD_OK, PD_NOT_CONVERGED = 0, 1
 _STATUS = {0: "PD_OK", 1: "PD_NOT_CONVERGED", -1: "PD_EINVAL", -2: "PD_ESINGULAR", -3: "PD_ECUDA",
@@ -149,7 +149,7 @@ def _ptr(t):
 class ParaDiag:
     """One ParaDiag-II context (pd_ctx) on the current CUDA device and stream.
 
-    op: ADE1D_DIRICHLET | WAVE1D_DIRICHLET | ADE2D_PERIODIC;  scheme: BE | CN | LEAPFROG.
+    op: ADE1D_DIRICHLET | WAVE1D_DIRICHLET | ADE2D_PERIODIC | WAVE2D_DIRICHLET;  scheme: BE | CN | LEAPFROG.
     Vectors are CUDA float64 tensors of shape [Nt, S_local] (S = nx*ny spatial dofs of this rank).
     rank=-1 with size>1 runs `size` virtual ranks of the sharded path on this GPU (global vectors).
     """

@@ -12,6 +12,8 @@
 #include "kernels.h"
 
 // partition plan: spatial slabs (1D x-ranges, 2D y-row ranges, in dofs) and frequency ranges per rank
+inline bool pd_is_2d(int op) { return op == PD_ADE2D_PERIODIC || op == PD_WAVE2D_DIRICHLET; }
+
 struct pd_plan {
   int P = 1;
   std::vector<long long> s_off, s_cnt;  // spatial dofs
@@ -75,6 +77,7 @@ struct pd_ctx {
   double* sn = nullptr;          // 2D: sin(2 pi k / N)
   double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
   pd_ytri_coef* ytri = nullptr;  // 2D: [F][N] cyclic Toeplitz y-pass constants (slab2d.cu ytri)
+  double* mu = nullptr;          // 2D Dirichlet: [M] DST eigenvalues (4 nu/h^2) sin^2(pi k / M), M = 2(N+1)
   bool use_ytri = false;
   pd_slab_params slab{};
   int slab_chunk = 1;

@@ -28,7 +28,7 @@ static cudaError_t dalloc(T** p, size_t n) {
 pd_plan pd_make_plan(int op, int nx, int ny, int nt, int P) {
   pd_plan pl;
   pl.P = P;
-  const bool two_d = op == PD_ADE2D_PERIODIC;
+  const bool two_d = pd_is_2d(op);
   const int ext = two_d ? ny : nx;
   const long long unit = two_d ? nx : 1;
   const int F = nt / 2 + 1;
@@ -64,13 +64,13 @@ extern "C" pd_status pd_partition(int op, int nx, int ny, int nt, int size, long
   return PD_OK;
 }
 
-static int hw_of(const pd_ctx* c) { return c->g.op == PD_ADE2D_PERIODIC ? c->g.nx : 1; }
+static int hw_of(const pd_ctx* c) { return pd_is_2d(c->g.op) ? c->g.nx : 1; }
 
 pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id) {
   const int P = c->size;
   c->plan = pd_make_plan(c->g.op, c->g.nx, c->g.ny, c->nt, P);
   const pd_plan& pl = c->plan;
-  const int ext = c->g.op == PD_ADE2D_PERIODIC ? c->g.ny : c->g.nx;
+  const int ext = pd_is_2d(c->g.op) ? c->g.ny : c->g.nx;
   if (P > ext) return fail(c, PD_EINVAL, "more ranks (%d) than spatial slabs (%d)", P, ext);
   if (P > c->F) return fail(c, PD_EINVAL, "more ranks (%d) than frequencies (%d)", P, c->F);
   const int hw = hw_of(c);
@@ -94,7 +94,7 @@ pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id) {
     sh.F = pl.f_cnt[p];
     sh.f0 = pl.f_off[p];
     sh.sten = c->sten;
-    if (c->g.op == PD_ADE2D_PERIODIC) {
+    if (pd_is_2d(c->g.op)) {
       sh.sten.nx = c->g.nx;
       sh.sten.ny = sh.ext;
     } else {

@@ -80,6 +80,11 @@ struct pd_ytri_coef {
   double2 sL;   // s^L
 };
 int pd_slab2d_ytri_supported(int n);
+// 2D homogeneous Dirichlet (PD_WAVE2D_DIRICHLET): N = 2^k - 1 interior nodes; tensor DST-I via FFTs of length
+// M = 2(N+1) of the odd extension; mu[k] = (4 nu/h^2) sin^2(pi k/M), k < M; tw: M-point twiddles
+int pd_slab2d_dst_supported(int n);
+cudaError_t pd_launch_slab2d_dst(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
+                                 const double* mu, const double2* tw, int chunk, cudaStream_t st, int* launches);
 int pd_slab2d_chunk(int n, int nfreq);
 // chunk = slabs per L2-resident chunk; *launches = kernels launched
 // one N x N complex slab in place: 2D FFT, multiply by tab[ky*N + kx] / N^2, inverse 2D FFT (tail map, tail.cu)

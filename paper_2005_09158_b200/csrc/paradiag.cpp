@@ -169,6 +169,7 @@ static void free_ctx(pd_ctx* c) {
   if (!c) return;
   pd_tail_free(c);
   if (c->ytri) cudaFree(c->ytri);
+  if (c->mu) cudaFree(c->mu);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
   for (void* p : ptrs)
@@ -216,6 +217,11 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   } else if (g->op == PD_ADE2D_PERIODIC) {
     if (g->nx != g->ny || !pd_slab2d_supported(g->nx))
       return fail(nullptr, PD_EINVAL, "2D grid must be N x N with N a power of two in [16, 1024]");
+  } else if (g->op == PD_WAVE2D_DIRICHLET) {
+    if (g->nx != g->ny || !pd_slab2d_dst_supported(g->nx))
+      return fail(nullptr, PD_EINVAL, "2D Dirichlet grid must be N x N with N + 1 a power of two in [16, 512]");
+    if (g->ax != 0.0 || g->ay != 0.0)
+      return fail(nullptr, PD_EINVAL, "2D Dirichlet operator is -nu Lap (ax = ay = 0: DST-I diagonalisation)");
   } else {
     return fail(nullptr, PD_EINVAL, "unknown operator %d", (int)g->op);
   }
@@ -246,8 +252,8 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     const pd_plan pl = pd_make_plan(g->op, g->nx, g->ny, nt, size);
     c->off = pl.s_off[rank];
     c->S = pl.s_cnt[rank];
-    c->nx_loc = g->op == PD_ADE2D_PERIODIC ? g->nx : pl.e_cnt[rank];
-    c->ny_loc = g->op == PD_ADE2D_PERIODIC ? pl.e_cnt[rank] : 1;
+    c->nx_loc = pd_is_2d(g->op) ? g->nx : pl.e_cnt[rank];
+    c->ny_loc = pd_is_2d(g->op) ? pl.e_cnt[rank] : 1;
   } else {
     c->nx_loc = g->nx;
     c->ny_loc = g->ny;
@@ -306,14 +312,48 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
 
   // ---- spatial operator ----
   pd_stencil& sp = c->sten;
-  sp.op = g->op == PD_ADE1D_DIRICHLET ? 0 : g->op == PD_WAVE1D_DIRICHLET ? 1 : 2;
+  sp.op = g->op == PD_ADE1D_DIRICHLET ? 0 : g->op == PD_WAVE1D_DIRICHLET ? 1 : g->op == PD_ADE2D_PERIODIC ? 2 : 3;
   sp.scheme = s == PD_BE ? 0 : s == PD_CN ? 1 : 2;
   sp.nx = c->nx_loc;
   sp.ny = c->ny_loc;
   sp.nt = nt;
   sp.dt = dt;
   sp.theta = s == PD_BE ? 1.0 : 0.5;
-  if (g->op != PD_ADE2D_PERIODIC) {
+  if (g->op == PD_WAVE2D_DIRICHLET) {
+    const int N = g->nx, M = 2 * (N + 1);
+    const double h = g->length / (N + 1);
+    sp.k2c = 4 * g->nu / (h * h);
+    sp.k2x_m = sp.k2x_p = sp.k2y_m = sp.k2y_p = -g->nu / (h * h);
+    std::vector<double> hmu(M);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < M; ++k) {
+      const long double sk = sinl(pi * k / M);
+      hmu[k] = (double)(4.0L * g->nu / ((long double)h * h) * sk * sk);
+    }
+    // singularity: min |lambda1 + lambda2 (mu_kx + mu_ky)| over the half spectrum and k = 1..N
+    long double worst = 1e300L;
+    int wn = -1;
+    for (int n = 0; n < c->F; ++n)
+      for (int kx = 1; kx <= N; ++kx)
+        for (int ky = 1; ky <= N; ky += (N > 64 ? 7 : 1)) {
+          const long double m = (long double)hmu[kx] + hmu[ky];
+          const long double r = std::abs(l1[n] + l2[n] * m) / (std::abs(l1[n]) + std::abs(l2[n]) * m + 1e-300L);
+          if (r < worst) {
+            worst = r;
+            wn = n;
+          }
+        }
+    if (worst < 1e-13L) {
+      free_ctx(c);
+      return fail(nullptr, PD_ESINGULAR, "shifted system singular at frequency n=%d (relative |den| %.3Le)", wn, worst);
+    }
+    std::vector<double2> htw = twiddles(M);
+    SETUP_CUDA(dalloc(&c->mu, M));
+    SETUP_CUDA(dalloc(&c->tw_s, M));
+    SETUP_CUDA(cudaMemcpy(c->mu, hmu.data(), M * sizeof(double), cudaMemcpyHostToDevice));
+    SETUP_CUDA(cudaMemcpy(c->tw_s, htw.data(), M * sizeof(double2), cudaMemcpyHostToDevice));
+    c->slab_chunk = pd_slab2d_chunk(N, c->F);
+  } else if (g->op != PD_ADE2D_PERIODIC) {
     const double h = g->length / (g->nx + 1);
     const double nu = g->nu, a = g->op == PD_ADE1D_DIRICHLET ? g->ax : 0.0;
     sp.sub = -nu / (h * h) - a / (2 * h);
@@ -532,7 +572,12 @@ static void phase_end(pd_ctx* c, int ph) {
 // Step (b) on a spectrum buffer holding frequencies [f0, f0 + nfreq) on full spatial rows
 pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   phase_begin(c, 1);
-  if (c->g.op == PD_ADE2D_PERIODIC) {
+  if (c->g.op == PD_WAVE2D_DIRICHLET) {
+    int nl = 0;
+    PD_CUDA(c, pd_launch_slab2d_dst(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->mu, c->tw_s, c->slab_chunk,
+                                    c->st, &nl));
+    c->launches += nl;
+  } else if (c->g.op == PD_ADE2D_PERIODIC) {
     int nl = 0;
     if (c->use_ytri)
       PD_CUDA(c, pd_launch_slab2d_ytri(Sh, c->g.nx, nfreq, f0, c->ytri, 1.0 / c->g.nx, c->tw_s, c->slab_chunk,

@@ -175,6 +175,133 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
 }
 
 // ---------------------------------------------------------------------------------------------
+// 2D homogeneous Dirichlet (Table T4A): K = -nu Lap_h is diagonalised by the tensor DST-I, mu_k = (4nu/h^2)
+// sin^2(pi k / M), M = 2(N+1).  A DST-I of length N is an FFT of length M of the odd extension
+// (0, z_1..z_N, 0, -z_N..-z_1): X[k] = -2i sum_j z_j sin(pi j k/(N+1)); X is itself odd, so after the forward
+// transform along y the spectrum is the odd extension of the DST coefficients and the column pass is
+// FFT -> divide by lambda1 + lambda2 (mu_kx + mu_ky) -> IFFT, exactly as the periodic pass.  Rows (x) and columns
+// (y) hold N values in HBM; the loaders build the extension, the storers keep positions 1..N.  Forward and
+// inverse along both directions give M^2 times the solution: the column pass scales by 1/M^2.
+PD_D double2 odd_ext(const double2* __restrict__ q, long long stride, int p, int N, int M) {
+  if (p == 0 || p == N + 1) return czero();
+  return p <= N ? __ldcg(q + (long long)(p - 1) * stride) : cneg(__ldcg(q + (long long)(M - p - 1) * stride));
+}
+
+// rows [blockIdx.x*C, +C) of the flattened chunk (total rows nrows = slabs * N), DST along x in place
+template <int M, bool INV>
+__global__ void __launch_bounds__(SlabCfg<M>::NTH, SlabCfg<M>::MINB)
+dst_rows_kernel(double2* __restrict__ base, long long nrows, const double2* __restrict__ tw) {
+  using T = SlabCfg<M>;
+  constexpr int C = T::C, NTH = T::NTH, N = M / 2 - 1, R0 = first_radix(M), RL = last_radix(M);
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw[M];
+  const long long row0 = (long long)blockIdx.x * C;
+  load_table(s_tw, tw, M);
+  __syncthreads();
+  fft_io<M, C, INV, true, NTH, false, false>(
+      sm, s_tw,
+      [&](int j, auto st, int c, double2* v) {
+        const bool ok = row0 + c < nrows;
+        const double2* q = base + (row0 + c) * N;
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = ok ? odd_ext(q, 1, j + m * decltype(st)::value, N, M) : czero();
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        if (row0 + c >= nrows) return;
+        double2* q = base + (row0 + c) * N;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) {
+          const int k = j + m * decltype(st)::value;
+          if (k >= 1 && k <= N) __stcg(q + k - 1, w[m]);
+        }
+      });
+}
+
+// columns [c0, c0 + C) of slab (slab0 + blockIdx.y): DST along y, divide, inverse DST along y, x 1/M^2
+template <int M>
+__global__ void __launch_bounds__(ColCfg<M>::NTH, ColCfg<M>::MINB)
+dst_cols_kernel(double2* __restrict__ Sh, int slab0, const double2* __restrict__ lam1, const double2* __restrict__ lam2,
+                const double* __restrict__ mu, const double2* __restrict__ tw) {
+  using T = ColCfg<M>;
+  constexpr int C = T::C, NTH = T::NTH, RM = T::RM, N = M / 2 - 1, R0 = first_radix(M, RM), RL = last_radix(M, RM);
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw[M];
+  const int n = slab0 + blockIdx.y;
+  const int c0 = blockIdx.x * C;
+  double2* slab = Sh + (long long)n * N * N + c0;
+  const double2 l1 = lam1[n], l2 = lam2[n];
+  const double inv = 1.0 / ((double)M * (double)M);
+  load_table(s_tw, tw, M);
+  __syncthreads();
+  fft_io<M, C, false, false, NTH, false, true, RM>(
+      sm, s_tw,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value;
+        const bool ok = c0 + c < N;
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = ok ? odd_ext(slab + c, N, j + m * s, N, M) : czero();
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value;
+        const double mx = __ldg(mu + c0 + c + 1);  // x-DST index k = element + 1
+        const int a = lin<M, C, false>(j, c);
+#pragma unroll
+        for (int m = 0; m < RL; ++m) {
+          const double muy = __ldg(mu + j + m * s);
+          sm[soff<s * C>(a, m)] = cscale(cmul(w[m], crcp_fast(cfma(l2, make_double2(mx + muy, 0.0), l1))), inv);
+        }
+      });
+  __syncthreads();
+  fft_io<M, C, true, false, NTH, true, false, RM>(
+      sm, s_tw,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value;
+        const int a = lin<M, C, false>(j, c);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = sm[soff<s * C>(a, m)];
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value;
+        if (c0 + c >= N) return;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) {
+          const int k = j + m * s;
+          if (k >= 1 && k <= N) __stcg(slab + c + (long long)(k - 1) * N, w[m]);
+        }
+      });
+}
+
+template <int M>
+cudaError_t dst_n(double2* Sh, int nfreq, const double2* lam1, const double2* lam2, const double* mu,
+                  const double2* tw, int chunk, cudaStream_t st, int* launches) {
+  using T = SlabCfg<M>;
+  constexpr int N = M / 2 - 1;
+  const int smr = smem_bytes<M>(), smc = smem_cols<M>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dst_rows_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dst_rows_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dst_cols_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smc);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int nl = 0;
+  for (int s0 = 0; s0 < nfreq; s0 += chunk) {
+    const int ns = nfreq - s0 < chunk ? nfreq - s0 : chunk;
+    double2* base = Sh + (long long)s0 * N * N;
+    const long long nrows = (long long)ns * N;
+    const unsigned row_ctas = (unsigned)((nrows + T::C - 1) / T::C);
+    dst_rows_kernel<M, false><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+    dst_cols_kernel<M><<<dim3((N + ColCfg<M>::C - 1) / ColCfg<M>::C, ns), ColCfg<M>::NTH, smc, st>>>(Sh, s0, lam1, lam2,
+                                                                                                    mu, tw);
+    dst_rows_kernel<M, true><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+    nl += 3;
+  }
+  if (launches) *launches = nl;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 // y-pass by cyclic Toeplitz tridiagonal solves (see kernels.h pd_ytri_coef).  8 columns per CTA, one warp per
 // column, L = N/32 consecutive rows per lane in registers; first-order recurrences carried across lanes by warp
 // affine scans, cyclic closures from the scan totals.  ~26 fp64 operations per complex element instead of the
@@ -351,6 +478,23 @@ cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, co
     case 256: return filter_n<256>(slab, tab, tw, st);
     case 512: return filter_n<512>(slab, tab, tw, st);
     case 1024: return filter_n<1024>(slab, tab, tw, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int pd_slab2d_dst_supported(int n) {
+  return n == 15 || n == 31 || n == 63 || n == 127 || n == 255 || n == 511;
+}
+
+cudaError_t pd_launch_slab2d_dst(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
+                                 const double* mu, const double2* tw, int chunk, cudaStream_t st, int* launches) {
+  switch (n) {
+    case 15: return dst_n<32>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
+    case 31: return dst_n<64>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
+    case 63: return dst_n<128>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
+    case 127: return dst_n<256>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
+    case 255: return dst_n<512>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
+    case 511: return dst_n<1024>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
     default: return cudaErrorInvalidValue;
   }
 }

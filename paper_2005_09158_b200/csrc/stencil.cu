@@ -150,18 +150,31 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
   if (warp < kTY) {
     y = y0 + warp;
     srow = warp + 1;
-  } else if (warp == kTY) {
+  }
+  // op 2: periodic wrap within the local rows (or the neighbour rank's halo); op 3: homogeneous Dirichlet
+  // (zero outside the domain; the neighbour rank's halo between shards)
+  const bool per = p.op == 2;
+  bool zrow = false;  // halo warp of a Dirichlet boundary: the row outside the domain is zero
+  if (warp == kTY) {
     y = y0 - 1;
     srow = 0;
-    if (y < 0) { y = ny - 1; hsrc = p.hlo; }
-  } else {
+    if (y < 0) {
+      y = ny - 1;
+      hsrc = p.hlo;
+      zrow = !per && !hsrc;
+    }
+  } else if (warp > kTY) {
     y = ylast + 1;
     srow = ylast - y0 + 2;
-    if (y >= ny) { y = 0; hsrc = p.hhi; }
+    if (y >= ny) {
+      y = 0;
+      hsrc = p.hhi;
+      zrow = !per && !hsrc;
+    }
   }
   const bool outw = warp < kTY && y <= ylast;
   const bool act = outw && xin;
-  const bool live = warp >= kTY || y <= ylast;  // rows whose combination is needed
+  const bool live = (warp >= kTY && !zrow) || (warp < kTY && y <= ylast);  // rows whose loads are needed
   const bool needL = outw && (lane == 0 || x == 0);
   const bool needR = outw && (lane == 31 || x == nx - 1);
   const int xl = x == 0 ? nx - 1 : x - 1, xp = x == nx - 1 ? 0 : x + 1;
@@ -175,13 +188,14 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
   auto ld = [&](const double* q, int n, int d) -> double { return (n >= 0 && live) ? q[d] : 0.0; };
   Hist c = {0.0, ld(pc - rstride, n0 - 1, 0), NT == 3 ? ld(pc - 2 * rstride, n0 - 2, 0) : 0.0};
   Hist L = {0.0, 0.0, 0.0}, R = {0.0, 0.0, 0.0};
-  if (needL) { L.h1 = ld(pc - rstride, n0 - 1, dl); if (NT == 3) L.h2 = ld(pc - 2 * rstride, n0 - 2, dl); }
-  if (needR) { R.h1 = ld(pc - rstride, n0 - 1, dr); if (NT == 3) R.h2 = ld(pc - 2 * rstride, n0 - 2, dr); }
+  const bool ldL = needL && (per || x != 0), ldR = needR && (per || x != nx - 1);  // Dirichlet: 0 outside
+  if (ldL) { L.h1 = ld(pc - rstride, n0 - 1, dl); if (NT == 3) L.h2 = ld(pc - 2 * rstride, n0 - 2, dl); }
+  if (ldR) { R.h1 = ld(pc - rstride, n0 - 1, dr); if (NT == 3) R.h2 = ld(pc - 2 * rstride, n0 - 2, dr); }
   const long long off = (long long)n0 * S + (long long)y * nx + x;
   const double* pb = b ? b + off : nullptr;
   double* po = out + off;
   // one-row prefetch
-  double nc = live ? pc[0] : 0.0, nl = needL ? pc[dl] : 0.0, nr = needR ? pc[dr] : 0.0;
+  double nc = live ? pc[0] : 0.0, nl = ldL ? pc[dl] : 0.0, nr = ldR ? pc[dr] : 0.0;
   double nb = (act && pb) ? pb[0] : 0.0;
   double acc = 0.0;
   int buf = 0;
@@ -191,12 +205,12 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
     if (n + 1 < n1) {
       pc += rstride;
       if (live) nc = pc[0];
-      if (needL) nl = pc[dl];
-      if (needR) nr = pc[dr];
+      if (ldL) nl = pc[dl];
+      if (ldR) nr = pc[dr];
       if (act && pb) nb = pb[S];
     }
     const double yc = comb<NT>(p, c);
-    if (live) ysh[buf][srow][lane] = yc;  // rows past ylast share the slot of the high halo row
+    if (live || warp >= kTY) ysh[buf][srow][lane] = yc;  // rows past ylast share the slot of the high halo row
     const double up = __shfl_up_sync(0xffffffffu, yc, 1);
     const double dn = __shfl_down_sync(0xffffffffu, yc, 1);
     const double yxm = needL ? comb<NT>(p, L) : up;
@@ -229,12 +243,24 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
 
 // ---------------- right-hand side ----------------
 // K v at spatial point s of a single time level (zero Dirichlet / periodic wrap)
+// 2D homogeneous Dirichlet neighbourhood (zero outside; halo rows of neighbour ranks in y)
+PD_D N2 load2_dir(const double* __restrict__ slab, int x, int y, int nx, int ny, const double* hl, const double* hr) {
+  N2 v;
+  v.c = slab[(long long)y * nx + x];
+  v.xm = x > 0 ? slab[(long long)y * nx + x - 1] : 0.0;
+  v.xp = x + 1 < nx ? slab[(long long)y * nx + x + 1] : 0.0;
+  v.ym = y > 0 ? slab[(long long)(y - 1) * nx + x] : (hl ? hl[x] : 0.0);
+  v.yp = y + 1 < ny ? slab[(long long)(y + 1) * nx + x] : (hr ? hr[x] : 0.0);
+  return v;
+}
+
 PD_D double applyK(const pd_stencil& p, const double* __restrict__ v, long long s, int which) {
-  const int hw = p.op == 2 ? p.nx : 1;
+  const int hw = p.op >= 2 ? p.nx : 1;
   const double* hl = p.hlo ? p.hlo + which * hw : nullptr;
   const double* hr = p.hhi ? p.hhi + which * hw : nullptr;
-  if (p.op == 2) {
-    const N2 h = load2(v, (int)(s % p.nx), (int)(s / p.nx), p.nx, p.ny, hl, hr);
+  if (p.op >= 2) {
+    const N2 h = p.op == 2 ? load2(v, (int)(s % p.nx), (int)(s / p.nx), p.nx, p.ny, hl, hr)
+                           : load2_dir(v, (int)(s % p.nx), (int)(s / p.nx), p.nx, p.ny, hl, hr);
     return p.k2c * h.c + p.k2x_m * h.xm + p.k2x_p * h.xp + p.k2y_m * h.ym + p.k2y_p * h.yp;
   }
   const N1 h = load1(v, (int)s, p.nx, hl, hr);
@@ -274,14 +300,14 @@ Taps taps_host(const pd_stencil& p) { return taps_of(p); }
 
 int pd_stencil_num_blocks(const pd_stencil& p) {
   const long long nz = (p.nt + kTC - 1) / kTC;
-  if (p.op == 2) return (int)(((p.nx + 31) / 32) * ((p.ny + kTY - 1) / kTY) * nz);
+  if (p.op >= 2) return (int)(((p.nx + 31) / 32) * ((p.ny + kTY - 1) / kTY) * nz);
   return (int)(((p.nx + kBX - 1) / kBX) * nz);
 }
 
 cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double* u, double* out, double* partial,
                               int* nblocks_out, cudaStream_t st) {
   if (nblocks_out) *nblocks_out = pd_stencil_num_blocks(p);
-  if (p.op == 2) {
+  if (p.op >= 2) {
     dim3 grid((unsigned)((p.nx + 31) / 32), (unsigned)((p.ny + kTY - 1) / kTY), (unsigned)((p.nt + kTC - 1) / kTC));
     pd_stencil q = p;
     const Taps t = taps_host(p);

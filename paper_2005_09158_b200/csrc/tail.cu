@@ -29,6 +29,11 @@ __global__ void head_G_kernel(pd_stencil p, pd_tail_g gc, const double* __restri
         const int ym = y == 0 ? ny - 1 : y - 1, yp = y == ny - 1 ? 0 : y + 1;
         k = p.k2c * tv[b] + p.k2x_m * t[(long long)y * nx + xm] + p.k2x_p * t[(long long)y * nx + xp] +
             p.k2y_m * t[(long long)ym * nx + x] + p.k2y_p * t[(long long)yp * nx + x];
+      } else if (p.op == 3) {  // 2D homogeneous Dirichlet
+        const int nx = p.nx, ny = p.ny;
+        const int x = (int)(i % nx), y = (int)(i / nx);
+        k = p.k2c * tv[b] + (x > 0 ? p.k2x_m * t[i - 1] : 0.0) + (x + 1 < nx ? p.k2x_p * t[i + 1] : 0.0) +
+            (y > 0 ? p.k2y_m * t[i - nx] : 0.0) + (y + 1 < ny ? p.k2y_p * t[i + nx] : 0.0);
       } else {
         k = p.dia * tv[b] + (i > 0 ? p.sub * t[i - 1] : 0.0) + (i + 1 < S ? p.sup * t[i + 1] : 0.0);
       }

@@ -33,6 +33,7 @@ pd_status tail_setup(pd_ctx* c) {
   auto& T = c->tail;
   if (T.ready) return PD_OK;
   if (c->dist_mode != 0) return fail(c, PD_EINVAL, "tail form: single-GPU contexts only");
+  if (c->g.op == PD_WAVE2D_DIRICHLET) return fail(c, PD_EINVAL, "tail form: not built for the 2D Dirichlet operator");
   const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
   if (c->nt < 2 * H) return fail(c, PD_EINVAL, "tail form needs Nt >= %d", 2 * H);
   const int nt = c->nt, F = c->F;

@@ -3,7 +3,7 @@ import numpy as np
 
 import workloads as W
 
-OPS = {W.ADE1D: 0, W.WAVE1D: 1, W.ADE2D: 2}
+OPS = {W.ADE1D: 0, W.WAVE1D: 1, W.ADE2D: 2, W.WAVE2D: 3}
 SCHEMES = {W.BE: 0, W.CN: 1, W.LF: 2}
 
 

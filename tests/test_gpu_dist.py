@@ -21,6 +21,7 @@ def _cases():
         ("ade2d_cn_P3", W.CONFIGS[4].scaled(nx=64, ny=64, nt=64, alpha=1e-3), 3),
         ("ade2d_cn_tf4_P4", W.CONFIGS[4].scaled(nx=32, ny=32, nt=2048, alpha=1e-3), 4),
         ("ade2d_be_tfx_P3_ragged", W.CONFIGS[3].scaled(nx=64, ny=64, nt=1024), 3),
+        ("wave2d_P3_ragged", W.t4a_config(32, 0.1), 3),
     ]
 
 

@@ -21,8 +21,8 @@ SOLVE_TOL = 1e-8
 
 
 def _cfg(op, scheme, nx, nt, alpha=1e-2, **kw):
-    base = {W.ADE1D: W.CONFIGS[0], W.WAVE1D: W.CONFIGS[2], W.ADE2D: W.CONFIGS[3]}[op]
-    if op == W.ADE2D:
+    base = {W.ADE1D: W.CONFIGS[0], W.WAVE1D: W.CONFIGS[2], W.ADE2D: W.CONFIGS[3], W.WAVE2D: W.t4a_config(32)}[op]
+    if op in (W.ADE2D, W.WAVE2D):
         return base.scaled(nx=nx, ny=nx, nt=nt, scheme=scheme, alpha=alpha, **kw)
     return base.scaled(nx=nx, nt=nt, scheme=scheme, alpha=alpha, **kw)
 
@@ -36,6 +36,9 @@ SMALL = [
     (W.ADE2D, W.BE, 256, 4), (W.ADE2D, W.CN, 512, 2),
     # time FFT with the x-FFT folded in (tfx.cu, Nt >= 1024): several x-rows per chunk, both residue cases
     (W.ADE2D, W.BE, 32, 1024), (W.ADE2D, W.CN, 64, 1024), (W.ADE2D, W.CN, 32, 4096),
+    # 2D homogeneous Dirichlet (Table T4A operator): tensor DST-I via odd-extension FFTs, ragged column tiles
+    (W.WAVE2D, W.LF, 15, 16), (W.WAVE2D, W.LF, 31, 64), (W.WAVE2D, W.LF, 63, 1024), (W.WAVE2D, W.BE, 31, 8),
+    (W.WAVE2D, W.LF, 255, 4),
 ]
 
 
@@ -45,7 +48,7 @@ def check_apply(cfg, r, z):
     by Cond_2(V) <= 1/alpha (eq 2.13); plus backward error ||P_alpha z - r|| <= 1e-10 ||r||."""
     z1 = spectral.apply_precond(cfg, r)
     tol = APPLY_TOL
-    if cfg.op == W.WAVE1D:  # the only family whose rounding floor approaches 1e-10 (resonant shifted systems)
+    if cfg.op in (W.WAVE1D, W.WAVE2D):  # the families whose rounding floor approaches 1e-10 (resonant systems)
         delta = rel(periodic.apply_precond_modal(cfg, r), z1)
         tol = max(APPLY_TOL, 4 * delta)
     err = rel(z, z1)
@@ -127,7 +130,8 @@ def test_apply_cfg4_full_properties():
 @pytest.mark.parametrize("op,scheme,nx,nt", [(W.ADE1D, W.BE, 63, 32), (W.ADE1D, W.CN, 1000, 70),
                                              (W.WAVE1D, W.LF, 333, 40), (W.ADE2D, W.BE, 64, 33),
                                              (W.ADE2D, W.CN, 32, 100), (W.ADE2D, W.CN, 16, 37),
-                                             (W.ADE2D, W.BE, 128, 130), (W.ADE2D, W.CN, 1024, 4)])
+                                             (W.ADE2D, W.BE, 128, 130), (W.ADE2D, W.CN, 1024, 4),
+                                             (W.WAVE2D, W.LF, 31, 32), (W.WAVE2D, W.BE, 63, 8)])
 def test_residual_matvec_rhs_match_oracle(op, scheme, nx, nt):
     nt_pow2 = 1 << (nt - 1).bit_length()
     cfg = _cfg(op, scheme, nx, nt_pow2)

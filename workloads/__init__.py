@@ -222,5 +222,5 @@ T4A_ITERS = {0.1: (3, 3, 3, 3), 1.0: (3, 7, 37, None)}      # None: "> 50"
 
 def t4a_config(label: int, alpha: float = 0.1, **kw) -> Config:
     c = Config(f"t4a_{label}", WAVE2D, nx=label - 1, ny=label - 1, nt=label, T=2.0, scheme=LF, alpha=alpha,
-               nu=1.0, solver="gmres", tol=1e-10, m=50, maxit=50, seed=0, source="exact_wave2d", init="exact_wave2d")
+               nu=1.0, solver="gmres", tol=1e-10, m=30, maxit=50, seed=0, source="exact_wave2d", init="exact_wave2d")
     return c.scaled(**kw) if kw else c
