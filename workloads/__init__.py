@@ -224,3 +224,15 @@ def t4a_config(label: int, alpha: float = 0.1, **kw) -> Config:
     c = Config(f"t4a_{label}", WAVE2D, nx=label - 1, ny=label - 1, nt=label, T=2.0, scheme=LF, alpha=alpha,
                nu=1.0, solver="gmres", tol=1e-10, m=30, maxit=50, seed=0, source="exact_wave2d", init="exact_wave2d")
     return c.scaled(**kw) if kw else c
+
+
+# Nonlinear ParaDiag-II by simplified Newton (eq 1.4-1.5, P:l.196-227): u_t + K u + g(u) = 0 on
+# (0,1), Dirichlet, K as config 1 (nu = 1e-2, a = 1), g(u) = c3 u^3 + c1 u (Allen-Cahn: c3 = 1, c1 = -1, reading
+# x5), u0 as config 1, f = 0, Crank-Nicolson, alpha = 1e-2, tol 1e-10.
+NL_REACTION = (1.0, -1.0)
+
+
+def nl_config(nx: int = 1023, nt: int = 1024, scheme: str = CN, **kw) -> Config:
+    c = Config("nl1", ADE1D, nx=nx, ny=1, nt=nt, T=1.0, scheme=scheme, alpha=1e-2, nu=1e-2, ax=1.0,
+               solver="newton", tol=1e-10, maxit=40, seed=1, init="sin_noise")
+    return c.scaled(**kw) if kw else c
