@@ -157,6 +157,18 @@ PD_API pd_status pd_solve_stationary_tail(pd_ctx* ctx, const double* b, double* 
  * Reports the true residual of the returned u (recomputed by the stencil at exit, as pd_solve_gmres). */
 PD_API pd_status pd_solve_gmres_tail(pd_ctx* ctx, const double* b, double* u, double tol, int m, int maxit, pd_report* rep);
 
+/* ---- nonlinear problems by simplified Newton (eq 1.4-1.5, P:l.196-227; oracle/nonlinear.py) ----
+ * pd_set_reaction: M U' + f(U) = 0 with f(U) = K U + g(U), g(u) = g3 u^3 + g1 u pointwise.  Afterwards pd_residual,
+ *   pd_matvec and pd_build_rhs are those of the nonlinear all-at-once system (B1 (x) I) u + (B2 (x) I) F(u) = b
+ *   (b_1 = U_0/dt - (1-theta) f(U_0)); (0, 0) restores the linear problem.  1D operators, PD_BE / PD_CN only
+ *   (PD_EINVAL otherwise).
+ * pd_solve_newton: u^{k+1} = u^k + P_alpha(u^k)^{-1} (b - (B1 u^k + B2 F(u^k))) with
+ *   P_alpha(u) = C1 (x) I + C2 (x) (K + diag((1/Nt) sum_n g'(U_n))) (the averaged Jacobian of P:l.214-216; its
+ *   shifted systems are tridiagonal but not Toeplitz: Thomas per frequency), until ||r|| <= tol ||b||.
+ *   u: initial guess in, solution out.  Single-GPU 1D theta-method contexts only. */
+PD_API pd_status pd_set_reaction(pd_ctx* ctx, double g3, double g1);
+PD_API pd_status pd_solve_newton(pd_ctx* ctx, const double* b, double* u, double tol, int maxit, pd_report* rep);
+
 /* HOST-buffer variants for end-to-end use: copy the HOST input(s) to device workspace on the context
  * stream (pinned memory recommended), run, copy the HOST output back, synchronise. */
 PD_API pd_status pd_apply_precond_host(pd_ctx* ctx, const double* r_host, double* z_host);

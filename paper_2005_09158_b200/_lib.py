@@ -79,6 +79,8 @@ def load_library(path: str | None = None):
         "pd_tail_map": (ip, [vp, vp, vp]),
         "pd_solve_stationary_tail": (ip, [vp, vp, vp, C.c_double, ip, C.POINTER(pd_report)]),
         "pd_solve_gmres_tail": (ip, [vp, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
+        "pd_set_reaction": (ip, [vp, C.c_double, C.c_double]),
+        "pd_solve_newton": (ip, [vp, vp, vp, C.c_double, ip, C.POINTER(pd_report)]),
         "pd_apply_precond_host": (ip, [vp, vp, vp]),
         "pd_solve_host": (ip, [vp, ip, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_kernel_launches": (C.c_longlong, [vp]),
@@ -281,6 +283,19 @@ class ParaDiag:
         u = torch.zeros(self.shape, dtype=torch.float64, device="cuda") if u is None else u
         rep, hist = self._report(maxit + 2)
         st = self._lib.pd_solve_gmres_tail(self._ctx, _ptr(b), _ptr(u), tol, m, maxit, C.byref(rep))
+        if raise_on_fail:
+            _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
+        return u, self._mk(st, rep, hist)
+
+    # ---- nonlinear (simplified Newton, include/paradiag.h) ----
+    def set_reaction(self, g3: float, g1: float):
+        _check(self._lib, self._ctx, self._lib.pd_set_reaction(self._ctx, float(g3), float(g1)))
+
+    def solve_newton(self, b, u=None, tol=1e-10, maxit=50, raise_on_fail=True):
+        import torch
+        u = torch.zeros(self.shape, dtype=torch.float64, device="cuda") if u is None else u
+        rep, hist = self._report(maxit + 2)
+        st = self._lib.pd_solve_newton(self._ctx, _ptr(b), _ptr(u), tol, maxit, C.byref(rep))
         if raise_on_fail:
             _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
         return u, self._mk(st, rep, hist)

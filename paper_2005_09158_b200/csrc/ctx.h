@@ -77,6 +77,8 @@ struct pd_ctx {
   double* sn = nullptr;          // 2D: sin(2 pi k / N)
   double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
   pd_ytri_coef* ytri = nullptr;  // 2D: [F][N] cyclic Toeplitz y-pass constants (slab2d.cu ytri)
+  double* nl_dbar = nullptr;     // NEXT-4: time-averaged reaction Jacobian [S]
+  double2* nl_cp = nullptr;      // NEXT-4: Thomas c' scratch [F][S]
   double* mu = nullptr;          // 2D Dirichlet: [M] DST eigenvalues (4 nu/h^2) sin^2(pi k / M), M = 2(N+1)
   bool use_ytri = false;
   pd_slab_params slab{};

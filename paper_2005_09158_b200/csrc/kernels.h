@@ -112,6 +112,7 @@ struct pd_stencil {
   const double* hlo;
   const double* hhi;
   double c1[3], c2[3];  // time taps (filled by pd_launch_stencil from scheme, dt, theta)
+  double g3, g1;        // 1D pointwise reaction g(u) = g3 u^3 + g1 u inside F(u) = K u + g(u) (NEXT-4; 0 = linear)
 };
 // out = b - A u (b != NULL) or out = A u (b == NULL); per-block partial sums of out^2 into partial[]
 cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double* u, double* out, double* partial,
@@ -146,3 +147,12 @@ cudaError_t pd_launch_r2c(const double* g, double2* z, long long n, cudaStream_t
 cudaError_t pd_launch_take_real(const double2* z, double* out, long long n, cudaStream_t st);
 // *flag = 1 if any x[i] != 0 (i < n), else unchanged (caller zeroes it)
 cudaError_t pd_launch_any_nonzero(const double* x, long long n, int* flag, cudaStream_t st);
+
+// ---- nonlinear ParaDiag-II, simplified Newton (nonlin.cu, oracle/nonlinear.py) ----
+// dbar[x] = (1/Nt) sum_n (3 g3 u_n(x)^2 + g1): the time-averaged reaction Jacobian (P:l.214-216)
+cudaError_t pd_launch_jac_avg(const double* u, double* dbar, int nt, long long S, double g3, double g1, cudaStream_t st);
+// Step (b) with J = K + diag(dbar): per frequency n the tridiagonal (lambda2 sub, lambda1 + lambda2 (dia + dbar_i),
+// lambda2 sup) by the Thomas algorithm (no pivoting: diagonally dominant at these shifts), one thread per
+// frequency; cp: [nfreq][nx] complex scratch
+cudaError_t pd_launch_thomas_shift(double2* Sh, int nx, int nfreq, const double2* lam1, const double2* lam2, double sub,
+                                   double dia, double sup, const double* dbar, double2* cp, cudaStream_t st);

@@ -170,6 +170,8 @@ static void free_ctx(pd_ctx* c) {
   pd_tail_free(c);
   if (c->ytri) cudaFree(c->ytri);
   if (c->mu) cudaFree(c->mu);
+  if (c->nl_dbar) cudaFree(c->nl_dbar);
+  if (c->nl_cp) cudaFree(c->nl_cp);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
   for (void* p : ptrs)

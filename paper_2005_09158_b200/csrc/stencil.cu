@@ -44,6 +44,7 @@ PD_D N1 load1(const double* __restrict__ row, int x, int nx, const double* hl, c
   return v;
 }
 
+template <bool NL>
 __global__ void __launch_bounds__(kBX, 4) stencil1d_kernel(pd_stencil p, const double* __restrict__ b,
                                                        const double* __restrict__ u, double* __restrict__ out,
                                                        double* __restrict__ partial) {
@@ -71,6 +72,10 @@ __global__ void __launch_bounds__(kBX, 4) stencil1d_kernel(pd_stencil p, const d
     const double yr = tp.c2[0] * h0.r + tp.c2[1] * h1.r + tp.c2[2] * h2.r;
     double Au = tp.c1[0] * h0.c + tp.c1[1] * h1.c + tp.c1[2] * h2.c;
     Au += p.sub * yl + p.dia * yc + p.sup * yr;
+    if constexpr (NL) {  // (B2 (x) I) g(u): F(u) = K u + g(u), g pointwise (eq 1.4)
+      auto g = [&](double v) { return v * fma(p.g3, v * v, p.g1); };
+      Au += tp.c2[0] * g(h0.c) + tp.c2[1] * g(h1.c) + tp.c2[2] * g(h2.c);
+    }
     if (act) {
       const long long idx = (long long)n * nx + x;
       const double v = b ? b[idx] - Au : Au;
@@ -288,7 +293,10 @@ __global__ void rhs_kernel(pd_stencil p, const double* __restrict__ u0, const do
     } else {
       // theta-method (P:l.321-323, reading c5): b_n = theta f_n + (1-theta) f_{n-1}; b_1 += (I/dt - (1-theta)K) U0
       if (f) v = p.theta * f[(long long)(n + 1) * S + s] + (1.0 - p.theta) * f[(long long)n * S + s];
-      if (n == 0) v += u0[s] / p.dt - (1.0 - p.theta) * applyK(p, u0, s, 0);
+      if (n == 0) {
+        v += u0[s] / p.dt - (1.0 - p.theta) * applyK(p, u0, s, 0);
+        if (p.g3 != 0.0 || p.g1 != 0.0) v -= (1.0 - p.theta) * u0[s] * fma(p.g3, u0[s] * u0[s], p.g1);  // f(U0)
+      }
     }
     b[i] = v;
   }
@@ -318,7 +326,10 @@ cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double
       stencil2d_kernel<2><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
   } else {
     dim3 grid((unsigned)((p.nx + kBX - 1) / kBX), (unsigned)((p.nt + kTC - 1) / kTC));
-    stencil1d_kernel<<<grid, kBX, 0, st>>>(p, b, u, out, partial);
+    if (p.g3 != 0.0 || p.g1 != 0.0)
+      stencil1d_kernel<true><<<grid, kBX, 0, st>>>(p, b, u, out, partial);
+    else
+      stencil1d_kernel<false><<<grid, kBX, 0, st>>>(p, b, u, out, partial);
   }
   return cudaGetLastError();
 }

@@ -71,11 +71,11 @@ def test_nl_gpu_matches_oracle(scheme, nx, nt):
     b = NL.rhs(cfg, RX, u0)
     ctx = make_ctx(cfg)
     ctx.set_reaction(*W.NL_REACTION)
-    bd = ctx.build_rhs_nl(to_dev(u0))
+    bd = ctx.build_rhs(to_dev(u0))
     assert rel(to_host(bd), b) < 1e-13
     u, rep = ctx.solve_newton(bd, tol=cfg.tol, maxit=cfg.maxit)
     u_ref, rep_ref = NL.solve_newton(cfg, RX, b)
     assert rep.converged and rep.iterations == rep_ref.iterations, (rep.history, rep_ref.history)
     assert rel(to_host(u), u_ref) < 1e-8
     for a, c in zip(rep.history, rep_ref.history):
-        assert abs(a - c) <= 1e-6 * c + 1e-14
+        assert abs(a - c) <= 1e-6 * c + 1e-12  # relative residuals: rounding floor ~1e-13
