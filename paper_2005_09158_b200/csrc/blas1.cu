@@ -59,12 +59,12 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
   for (long long t = lo + threadIdx.x; t < hi; t += kThreads) {
-    double2 yv = MODE == 3 ? czero() : reinterpret_cast<const double2*>(y)[t];
+    double2 yv = MODE >= 3 ? czero() : reinterpret_cast<const double2*>(y)[t];
     double2 xv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) xv[i] = ld2_keep(X.p[i], t);
     if constexpr (MODE >= 1) {
-      double2 nv = MODE == 3 ? czero() : make_double2(a * yv.x, a * yv.y);
+      double2 nv = MODE >= 3 ? czero() : make_double2(a * yv.x, a * yv.y);
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         nv.x = fma(X.c[i], xv[i].x, nv.x);
@@ -84,9 +84,9 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
   if (n & 1) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const long long t = n - 1;
-      double yv = MODE == 3 ? 0.0 : y[t];
+      double yv = MODE >= 3 ? 0.0 : y[t];
       if constexpr (MODE >= 1) {
-        double nv = MODE == 3 ? 0.0 : a * yv;
+        double nv = MODE >= 3 ? 0.0 : a * yv;
 #pragma unroll
         for (int i = 0; i < K; ++i) nv = fma(X.c[i], X.p[i][t], nv);
         yv = nv;
@@ -164,6 +164,7 @@ cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coe
   if (mode == 0) return krylov_launch<0>(pk, k, a, y, n, partial, st);
   if (mode == 1) return krylov_launch<1>(pk, k, a, y, n, partial, st);
   if (mode == 2) return krylov_launch<2>(pk, k, a, y, n, partial, st);
+  if (mode == 4) return krylov_launch<4>(pk, k, a, y, n, partial, st);
   return krylov_launch<3>(pk, k, a, y, n, partial, st);
 }
 

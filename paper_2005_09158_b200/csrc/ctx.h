@@ -97,6 +97,7 @@ struct pd_ctx {
   int gm_m = 0;
   std::vector<double*> V;
   double* zvec = nullptr;
+  double* gm_head = nullptr;     // head-sized work vector of the corner-identity GMRES path
   // host-buffer staging
   double* stage_a = nullptr;
   double* stage_b = nullptr;
@@ -166,6 +167,7 @@ pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double*
                       long long n, double* host_out);
 extern "C" void pd_report_push(pd_report* rep, double v);
 void pd_tail_free(pd_ctx* c);
+void pd_corner_coefs(const pd_ctx* c, pd_tail_g* gc);
 pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0);
 pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S);
 pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate);

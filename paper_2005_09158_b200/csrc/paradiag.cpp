@@ -171,6 +171,7 @@ static void free_ctx(pd_ctx* c) {
   if (c->ytri) cudaFree(c->ytri);
   if (c->mu) cudaFree(c->mu);
   if (c->nl_dbar) cudaFree(c->nl_dbar);
+  if (c->gm_head) cudaFree(c->gm_head);
   if (c->nl_cp) cudaFree(c->nl_cp);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
@@ -847,6 +848,18 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
   std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m), coef(m + 1), sc(m + 1);
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
   const double* const* Xp = c->V.data();
+  // corner identity path (single GPU, linear operator); PD_GMRES_MATVEC=1 keeps the explicit matvec
+  pd_tail_g gcorner{};
+  pd_corner_coefs(c, &gcorner);
+  const bool corner = c->dist_mode == 0 && c->sten.g3 == 0.0 && c->sten.g1 == 0.0 && gcorner.H >= 1 &&
+                      c->nt >= 2 * gcorner.H && getenv("PD_GMRES_MATVEC") == nullptr;
+  const long long hn_len = (long long)gcorner.H * c->S;
+  std::vector<double> eh(m + 1);
+  double* dhead = nullptr;
+  if (corner) {
+    if (!c->gm_head) PD_CUDA(c, dalloc(&c->gm_head, (size_t)(2 * c->S + 2)));
+    dhead = c->gm_head;
+  }
   while (!conv && its < maxit) {
     sc[0] = 1.0 / beta;
     std::fill(gv.begin(), gv.end(), 0.0);
@@ -858,21 +871,48 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
       if (s != PD_OK) return s;
       ++its;
       double* w = c->V[j + 1];
-      s = pd_stencil_impl(c, nullptr, c->zvec, w, nullptr);
-      if (s != PD_OK) return s;
-      // CGS2: h_i = <V_i, w> = sc_i sc_j <X_i, w_raw>;  w_raw -= sum (h_i sc_i / sc_j) X_i  (fused with 2nd dots)
-      s = krylov_impl(c, 0, Xp, nullptr, j + 1, 0.0, w, h.data());
-      if (s != PD_OK) return s;
-      for (int i = 0; i <= j; ++i) {
-        h[i] *= sc[i] * sc[j];
-        coef[i] = -h[i] * sc[i] / sc[j];
-      }
-      s = krylov_impl(c, 1, Xp, coef.data(), j + 1, 1.0, w, h2.data());
-      if (s != PD_OK) return s;
-      for (int i = 0; i <= j; ++i) {
-        h2[i] *= sc[i] * sc[j];
-        coef[i] = -h2[i] * sc[i] / sc[j];
-        h[i] += h2[i];
+      if (corner) {
+        // A P^{-1} X_j = X_j - E_H G tail(P^{-1} X_j)  ((P - A) touches only head rows x tail columns, the identity
+        // behind the tail form): the matvec sweep disappears and, the basis being orthonormal, the first CGS pass is
+        // h_i = delta_ij - sc_i sc_j <X_i[head], G tail>: head-only dots.  The second pass measures the true
+        // projections of the assembled w as before, so orthogonality is enforced to working precision.
+        PD_LAUNCH(c, pd_launch_head_G(c->sten, gcorner, c->zvec + (long long)(c->nt - gcorner.H) * c->S, dhead,
+                                      c->S, c->st));
+        s = pd_krylov_n(c, 0, Xp, nullptr, j + 1, 0.0, dhead, hn_len, eh.data());  // <X_i[head], G tail>
+        if (s != PD_OK) return s;
+        for (int i = 0; i <= j; ++i) {
+          h[i] = (i == j ? 1.0 : 0.0) - sc[i] * sc[j] * eh[i];
+          coef[i] = -h[i] * sc[i] / sc[j];
+        }
+        coef[j] += 1.0;  // w_raw = X_j + E_H delta - sum (h_i sc_i / sc_j) X_i
+        s = pd_krylov_n(c, 4, Xp, coef.data(), j + 1, 0.0, w, n, h2.data());  // written fresh, dots of the X part
+        if (s != PD_OK) return s;
+        const double* hx[2] = {w, dhead};
+        const double hc[2] = {1.0, -1.0};
+        s = pd_krylov_n(c, 3, hx, hc, 2, 0.0, w, hn_len, nullptr);  // + E_H delta (delta = -G tail)
+        if (s != PD_OK) return s;
+        for (int i = 0; i <= j; ++i) {
+          h2[i] = sc[i] * sc[j] * (h2[i] - eh[i]);
+          coef[i] = -h2[i] * sc[i] / sc[j];
+          h[i] += h2[i];
+        }
+      } else {
+        s = pd_stencil_impl(c, nullptr, c->zvec, w, nullptr);
+        if (s != PD_OK) return s;
+        // CGS2: h_i = <V_i, w> = sc_i sc_j <X_i, w_raw>;  w_raw -= sum (h_i sc_i / sc_j) X_i  (fused with 2nd dots)
+        s = krylov_impl(c, 0, Xp, nullptr, j + 1, 0.0, w, h.data());
+        if (s != PD_OK) return s;
+        for (int i = 0; i <= j; ++i) {
+          h[i] *= sc[i] * sc[j];
+          coef[i] = -h[i] * sc[i] / sc[j];
+        }
+        s = krylov_impl(c, 1, Xp, coef.data(), j + 1, 1.0, w, h2.data());
+        if (s != PD_OK) return s;
+        for (int i = 0; i <= j; ++i) {
+          h2[i] *= sc[i] * sc[j];
+          coef[i] = -h2[i] * sc[i] / sc[j];
+          h[i] += h2[i];
+        }
       }
       double ww = 0;
       s = krylov_impl(c, 2, Xp, coef.data(), j + 1, 1.0, w, &ww);

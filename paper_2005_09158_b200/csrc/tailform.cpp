@@ -29,16 +29,15 @@ cudaError_t dalloc_c(double2** p, size_t n) { return cudaMalloc(reinterpret_cast
 
 long long hs(const pd_ctx* c) { return (long long)c->tail.H * c->S; }
 
-pd_status tail_setup(pd_ctx* c) {
-  auto& T = c->tail;
-  if (T.ready) return PD_OK;
-  if (c->dist_mode != 0) return fail(c, PD_EINVAL, "tail form: single-GPU contexts only");
-  if (c->g.op == PD_WAVE2D_DIRICHLET) return fail(c, PD_EINVAL, "tail form: not built for the 2D Dirichlet operator");
+}  // namespace
+
+// (P_alpha - A) = E_H G U_tail: H and the coefficients of G from the alpha-corner of the time first columns
+void pd_corner_coefs(const pd_ctx* c, pd_tail_g* gc) {
   const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
-  if (c->nt < 2 * H) return fail(c, PD_EINVAL, "tail form needs Nt >= %d", 2 * H);
-  const int nt = c->nt, F = c->F;
+  const int nt = c->nt;
   const double dt = c->dt, al = c->alpha;
-  // time first columns (oracle problems.time_first_columns): taps 0..2
+  pd_tail_g T{};
+  T.H = H;
   double c1[3] = {0, 0, 0}, c2[3] = {0, 0, 0};
   if (c->scheme == PD_LEAPFROG) {
     c1[0] = 1.0 / (dt * dt); c1[1] = -2.0 / (dt * dt); c1[2] = 1.0 / (dt * dt);
@@ -49,16 +48,29 @@ pd_status tail_setup(pd_ctx* c) {
     c2[0] = th; c2[1] = 1.0 - th;
   }
   // alpha-corner of the alpha-circulants: entry (a, j) with a < j, j = Nt-H+b, tap k = a - j + Nt = a - b + H
-  T.gc = pd_tail_g{};
-  T.gc.H = H;
   for (int a = 0; a < H; ++a)
     for (int b = 0; b < H; ++b) {
       const int j = nt - H + b, k = a - b + H;
       if (a < j && k >= 1 && k <= 2) {
-        T.gc.pI[a][b] = al * c1[k];
-        T.gc.pK[a][b] = al * c2[k];
+        T.pI[a][b] = al * c1[k];
+        T.pK[a][b] = al * c2[k];
       }
     }
+  *gc = T;
+}
+
+namespace {
+
+pd_status tail_setup(pd_ctx* c) {
+  auto& T = c->tail;
+  if (T.ready) return PD_OK;
+  if (c->dist_mode != 0) return fail(c, PD_EINVAL, "tail form: single-GPU contexts only");
+  if (c->g.op == PD_WAVE2D_DIRICHLET) return fail(c, PD_EINVAL, "tail form: not built for the 2D Dirichlet operator");
+  const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
+  if (c->nt < 2 * H) return fail(c, PD_EINVAL, "tail form needs Nt >= %d", 2 * H);
+  const int nt = c->nt, F = c->F;
+  const double dt = c->dt, al = c->alpha;
+  pd_corner_coefs(c, &T.gc);
   // economical Step (a) coefficients and last-H-row Step (c) weights (long double, closed form)
   typedef std::complex<long double> cld;
   const long double pi = 3.141592653589793238462643383279502884L;

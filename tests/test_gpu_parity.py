@@ -252,3 +252,20 @@ def test_apply_2d_fft_column_pass_matches_oracle(nx, nt, monkeypatch):
     r = W.random_vector(cfg, seed=nx + nt)
     z = to_host(make_ctx(cfg).apply_precond(to_dev(r)))
     check_apply(cfg, r, z)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3"])
+def test_gmres_corner_identity_equals_matvec_path(name, monkeypatch):
+    """GMRES forms w = A P^{-1} v as v - E_H G tail(P^{-1} v) with an algebraic first CGS pass (single GPU); the
+    explicit-matvec path (PD_GMRES_MATVEC=1, used by the sharded executor) gives the same counts and solution."""
+    cfg = W.BY_NAME[name]
+    u0, v0, f = W.initial_u0(cfg), W.initial_v0(cfg), W.source_samples(cfg)
+    b = problems.rhs(cfg, u0, v0, f)
+    ctx = make_ctx(cfg)
+    u1, r1 = ctx.solve_gmres(to_dev(b), tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
+    monkeypatch.setenv("PD_GMRES_MATVEC", "1")
+    u2, r2 = ctx.solve_gmres(to_dev(b), tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
+    assert r1.iterations == r2.iterations and r1.converged and r2.converged
+    assert rel(to_host(u1), to_host(u2)) < 1e-10
+    for a, c in zip(r1.history, r2.history):
+        assert abs(a - c) <= 1e-6 * c + 1e-14
