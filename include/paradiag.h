@@ -170,7 +170,10 @@ PD_API pd_status pd_set_reaction(pd_ctx* ctx, double g3, double g1);
 PD_API pd_status pd_solve_newton(pd_ctx* ctx, const double* b, double* u, double tol, int maxit, pd_report* rep);
 
 /* HOST-buffer variants for end-to-end use: copy the HOST input(s) to device workspace on the context
- * stream (pinned memory recommended), run, copy the HOST output back, synchronise. */
+ * stream (pinned memory recommended), run, copy the HOST output back, synchronise.
+ * pd_solve_host: solver 0 stationary, 1 GMRES; OR-ing PD_SOLVE_ZERO_GUESS starts from u = 0 without copying
+ * u_host in (u_host is then output only: one host->device copy per solve instead of two). */
+#define PD_SOLVE_ZERO_GUESS 16
 PD_API pd_status pd_apply_precond_host(pd_ctx* ctx, const double* r_host, double* z_host);
 PD_API pd_status pd_solve_host(pd_ctx* ctx, int solver /*0 stationary, 1 gmres*/, const double* b_host,
                         double* u_host, double tol, int m, int maxit, pd_report* rep);

@@ -98,6 +98,8 @@ struct pd_ctx {
   std::vector<double*> V;
   double* zvec = nullptr;
   double* gm_head = nullptr;     // head-sized work vector of the corner-identity GMRES path
+  int* gm_flag = nullptr;        // zero-initial-guess check
+  int* gm_hflag = nullptr;
   // host-buffer staging
   double* stage_a = nullptr;
   double* stage_b = nullptr;

@@ -172,6 +172,8 @@ static void free_ctx(pd_ctx* c) {
   if (c->mu) cudaFree(c->mu);
   if (c->nl_dbar) cudaFree(c->nl_dbar);
   if (c->gm_head) cudaFree(c->gm_head);
+  if (c->gm_flag) cudaFree(c->gm_flag);
+  if (c->gm_hflag) cudaFreeHost(c->gm_hflag);
   if (c->nl_cp) cudaFree(c->nl_cp);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
@@ -839,15 +841,35 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     return PD_OK;
   }
   // Basis kept scaled: V_i = sc[i] * X_i with X_i = c->V[i] in memory, so normalising costs no sweep.
+  // Zero initial guess (checked on the device, single GPU): r0 = b exactly, so the first cycle reads X_0 = b in
+  // place of a residual sweep; a restart writes the true residual into c->V[0].
+  std::vector<const double*> Xv(c->V.begin(), c->V.end());
   double rr = 0;
-  s = pd_stencil_impl(c, b, u, c->V[0], &rr);  // X_0 = r = b - A u
-  if (s != PD_OK) return s;
+  bool u_zero = false;
+  if (c->dist_mode == 0) {
+    if (!c->gm_flag) {
+      PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->gm_flag), sizeof(int)));
+      PD_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->gm_hflag), sizeof(int)));
+    }
+    PD_CUDA(c, cudaMemsetAsync(c->gm_flag, 0, sizeof(int), c->st));
+    PD_LAUNCH(c, pd_launch_any_nonzero(u, n, c->gm_flag, c->st));
+    PD_CUDA(c, cudaMemcpyAsync(c->gm_hflag, c->gm_flag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    PD_CUDA(c, cudaStreamSynchronize(c->st));
+    u_zero = *c->gm_hflag == 0;
+  }
+  if (u_zero) {
+    Xv[0] = b;
+    rr = bb;
+  } else {
+    s = pd_stencil_impl(c, b, u, c->V[0], &rr);  // X_0 = r = b - A u
+    if (s != PD_OK) return s;
+  }
   double beta = std::sqrt(rr);
   int its = 0;
   bool conv = beta <= tol * bnorm, breakdown = false;
   std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m), coef(m + 1), sc(m + 1);
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
-  const double* const* Xp = c->V.data();
+  const double* const* Xp = Xv.data();
   // corner identity path (single GPU, linear operator); PD_GMRES_MATVEC=1 keeps the explicit matvec
   pd_tail_g gcorner{};
   pd_corner_coefs(c, &gcorner);
@@ -867,7 +889,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     int kk = 0;
     for (int j = 0; j < m; ++j) {
       // w_raw = A P^{-1} X_j;  true w = sc[j] * w_raw
-      s = pd_apply_impl(c, c->V[j], c->zvec, 0);
+      s = pd_apply_impl(c, Xv[j], c->zvec, 0);
       if (s != PD_OK) return s;
       ++its;
       double* w = c->V[j + 1];
@@ -953,6 +975,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     s = pd_apply_impl(c, c->zvec, u, 1);
     if (s != PD_OK) return s;
     s = pd_stencil_impl(c, b, u, c->V[0], &rr);  // true residual, also the restart vector X_0
+    Xv[0] = c->V[0];
     if (s != PD_OK) return s;
     beta = std::sqrt(rr);
     conv = beta <= tol * bnorm;
@@ -997,7 +1020,11 @@ pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, dou
   if (s != PD_OK) return s;
   const size_t bytes = sizeof(double) * c->nt * c->S;
   PD_CUDA(c, cudaMemcpyAsync(c->stage_a, bh, bytes, cudaMemcpyHostToDevice, c->st));
-  PD_CUDA(c, cudaMemcpyAsync(c->stage_b, uh, bytes, cudaMemcpyHostToDevice, c->st));
+  if (solver & PD_SOLVE_ZERO_GUESS)
+    PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
+  else
+    PD_CUDA(c, cudaMemcpyAsync(c->stage_b, uh, bytes, cudaMemcpyHostToDevice, c->st));
+  solver &= ~PD_SOLVE_ZERO_GUESS;
   s = solver == 0 ? pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep)
                   : pd_solve_gmres(c, c->stage_a, c->stage_b, tol, m, maxit, rep);
   if (s < 0) return s;

@@ -232,8 +232,18 @@ def test_host_buffer_paths():
     bh = torch.from_numpy(b).pin_memory()
     uh = torch.zeros_like(bh).pin_memory()
     _, rep = ctx.solve_host(1, bh, uh, cfg.tol, cfg.m, cfg.maxit)
-    _, rep_ref = solvers.solve_gmres(cfg, b)
+    u_ref, rep_ref = solvers.solve_gmres(cfg, b)
     assert rep.converged and rep.iterations == rep_ref.iterations
+    # PD_SOLVE_ZERO_GUESS: u_host is output only (garbage in is ignored)
+    uh2 = torch.full_like(bh, float("nan")).pin_memory()
+    _, rep2 = ctx.solve_host(1 | 16, bh, uh2, cfg.tol, cfg.m, cfg.maxit)
+    assert rep2.iterations == rep_ref.iterations and rel(uh2.numpy(), u_ref) < SOLVE_TOL
+    # stationary through the host ABI, non-zero initial guess honoured
+    u0 = np.random.default_rng(3).standard_normal(b.shape)
+    uh3 = torch.from_numpy(u0.copy()).pin_memory()
+    _, rep3 = ctx.solve_host(0, bh, uh3, cfg.tol, cfg.m, 60)
+    u_s, rep_s = solvers.solve_stationary(cfg, b, u0=u0, tol=cfg.tol, maxit=60)
+    assert rep3.iterations == rep_s.iterations and rel(uh3.numpy(), u_s) < SOLVE_TOL
 
 
 def test_spectra_match_oracle():
