@@ -12,55 +12,108 @@
 
 namespace {
 
-__global__ void jac_avg_kernel(const double* __restrict__ u, double* __restrict__ dbar, int nt, long long S, double g3,
-                               double g1) {
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < S; x += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int n = 0; n < nt; ++n) {
-      const double v = u[(long long)n * S + x];
-      s = fma(3.0 * g3 * v, v, s);
+// 64 nodes x 4 time quarters per CTA; each thread keeps 4 independent partial sums, the quarters are combined in a
+// fixed order (deterministic)
+__global__ void __launch_bounds__(256) jac_avg_kernel(const double* __restrict__ u, double* __restrict__ dbar, int nt,
+                                                      long long S, double g3, double g1) {
+  __shared__ double part[4][64];
+  const int xl = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const long long x = (long long)blockIdx.x * 64 + xl;
+  const int n0 = q * nt / 4, n1 = (q + 1) * nt / 4;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (x < S) {
+    int n = n0;
+    for (; n + 4 <= n1; n += 4) {
+      const double v0 = u[(long long)n * S + x], v1 = u[(long long)(n + 1) * S + x];
+      const double v2 = u[(long long)(n + 2) * S + x], v3 = u[(long long)(n + 3) * S + x];
+      s0 = fma(v0, v0, s0);
+      s1 = fma(v1, v1, s1);
+      s2 = fma(v2, v2, s2);
+      s3 = fma(v3, v3, s3);
     }
-    dbar[x] = s / nt + g1;
+    for (; n < n1; ++n) {
+      const double v = u[(long long)n * S + x];
+      s0 = fma(v, v, s0);
+    }
   }
+  part[q][xl] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (q == 0 && x < S) dbar[x] = 3.0 * g3 * (((part[0][xl] + part[1][xl]) + (part[2][xl] + part[3][xl])) / nt) + g1;
 }
 
-__global__ void thomas_shift_kernel(double2* __restrict__ Sh, int N, int F, const double2* __restrict__ lam1,
-                                    const double2* __restrict__ lam2, double sub, double dia, double sup,
-                                    const double* __restrict__ dbar, double2* __restrict__ cp) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= F) return;
-  const double2 l1 = lam1[n], l2 = lam2[n];
+// 32 frequencies per CTA (one warp), lane = frequency.  Rows are walked in tiles of 32: a tile of d (32 rows x 32
+// frequencies) is loaded coalesced (one frequency's 32 consecutive rows per instruction) and transposed through
+// shared memory, each lane runs the sequential Thomas recurrence over its frequency's 32 rows, and the tile goes
+// back the same way.  c' is kept in a scratch row per frequency (tiled the same way).
+constexpr int kTT = 32;
+__global__ void __launch_bounds__(32) thomas_shift_kernel(double2* __restrict__ Sh, int N, int F,
+                                                          const double2* __restrict__ lam1,
+                                                          const double2* __restrict__ lam2, double sub, double dia,
+                                                          double sup, const double* __restrict__ dbar,
+                                                          double2* __restrict__ cp) {
+  __shared__ double2 td[kTT][kTT + 1], tc[kTT][kTT + 1];  // [row][frequency]
+  const int lane = threadIdx.x;
+  const int f0 = blockIdx.x * kTT;
+  const int n = f0 + lane;
+  const bool on = n < F;
+  const double2 l1 = on ? lam1[n] : make_double2(1.0, 0.0), l2 = on ? lam2[n] : czero();
   const double2 a = cscale(l2, sub), c = cscale(l2, sup);
-  double2* d = Sh + (long long)n * N;
-  double2* cr = cp + (long long)n * N;
-  // forward: m_i = b_i - a c'_{i-1};  c'_i = c / m_i;  d'_i = (d_i - a d'_{i-1}) / m_i
+  auto load_tile = [&](double2 (*t)[kTT + 1], const double2* base, int i0) {
+    for (int k = 0; k < kTT; ++k) {  // frequency f0 + k, rows i0 + lane
+      const bool ok = f0 + k < F && i0 + lane < N;
+      t[lane][k] = ok ? base[(long long)(f0 + k) * N + i0 + lane] : czero();
+    }
+  };
+  auto store_tile = [&](double2 (*t)[kTT + 1], double2* base, int i0) {
+    for (int k = 0; k < kTT; ++k)
+      if (f0 + k < F && i0 + lane < N) base[(long long)(f0 + k) * N + i0 + lane] = t[lane][k];
+  };
+  // forward elimination: m_i = b_i - a c'_{i-1};  c'_i = c / m_i;  d'_i = (d_i - a d'_{i-1}) / m_i
   double2 cprev = czero(), dprev = czero();
-  for (int i = 0; i < N; ++i) {
-    const double2 bi = cfma(l2, make_double2(dia + __ldg(dbar + i), 0.0), l1);
-    const double2 im = crcp(csub(bi, cmul(a, cprev)));
-    cprev = cmul(c, im);
-    dprev = cmul(csub(d[i], cmul(a, dprev)), im);
-    cr[i] = cprev;
-    d[i] = dprev;
+  for (int i0 = 0; i0 < N; i0 += kTT) {
+    load_tile(td, Sh, i0);
+    __syncwarp();
+    const int iend = min(kTT, N - i0);
+    for (int r = 0; r < iend; ++r) {
+      const double2 bi = cfma(l2, make_double2(dia + __ldg(dbar + i0 + r), 0.0), l1);
+      const double2 im = crcp_fast(csub(bi, cmul(a, cprev)));
+      cprev = cmul(c, im);
+      dprev = cmul(csub(td[r][lane], cmul(a, dprev)), im);
+      tc[r][lane] = cprev;
+      td[r][lane] = dprev;
+    }
+    __syncwarp();
+    store_tile(td, Sh, i0);
+    store_tile(tc, cp, i0);
+    __syncwarp();
   }
-  // back substitution: x_{N-1} = d'_{N-1};  x_i = d'_i - c'_i x_{i+1}
-  double2 xn = dprev;
-  for (int i = N - 2; i >= 0; --i) {
-    xn = csub(d[i], cmul(cr[i], xn));
-    d[i] = xn;
+  // back substitution over the tiles in reverse: x_{N-1} = d'_{N-1};  x_i = d'_i - c'_i x_{i+1}
+  double2 xn = czero();
+  const int last0 = ((N - 1) / kTT) * kTT;
+  for (int i0 = last0; i0 >= 0; i0 -= kTT) {
+    load_tile(td, Sh, i0);
+    load_tile(tc, cp, i0);
+    __syncwarp();
+    const int iend = min(kTT, N - i0);
+    for (int r = iend - 1; r >= 0; --r) {
+      xn = (i0 + r == N - 1) ? td[r][lane] : csub(td[r][lane], cmul(tc[r][lane], xn));
+      td[r][lane] = xn;
+    }
+    __syncwarp();
+    store_tile(td, Sh, i0);
+    __syncwarp();
   }
 }
 
 }  // namespace
 
 cudaError_t pd_launch_jac_avg(const double* u, double* dbar, int nt, long long S, double g3, double g1, cudaStream_t st) {
-  const unsigned g = (unsigned)std::min<long long>((S + 255) / 256, 148 * 8);
-  jac_avg_kernel<<<g, 256, 0, st>>>(u, dbar, nt, S, g3, g1);
+  jac_avg_kernel<<<(unsigned)((S + 63) / 64), 256, 0, st>>>(u, dbar, nt, S, g3, g1);
   return cudaGetLastError();
 }
 
 cudaError_t pd_launch_thomas_shift(double2* Sh, int nx, int nfreq, const double2* lam1, const double2* lam2, double sub,
                                    double dia, double sup, const double* dbar, double2* cp, cudaStream_t st) {
-  thomas_shift_kernel<<<(nfreq + 63) / 64, 64, 0, st>>>(Sh, nx, nfreq, lam1, lam2, sub, dia, sup, dbar, cp);
+  thomas_shift_kernel<<<(nfreq + kTT - 1) / kTT, kTT, 0, st>>>(Sh, nx, nfreq, lam1, lam2, sub, dia, sup, dbar, cp);
   return cudaGetLastError();
 }

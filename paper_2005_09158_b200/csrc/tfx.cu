@@ -37,6 +37,12 @@ constexpr int kRM = 8;  // the N1 = 8 point DFTs: one radix-8 pass
 #define PD_TFX_S1_RM 16 // radix cap of the N2-point stage FFTs (tf4_stages.cuh)
 #endif
 constexpr int kRX = PD_TFX_RM;
+#ifndef PD_TFX_MINB
+#define PD_TFX_MINB 2   // min resident CTAs per SM (1: 144 regs, one CTA, measured 20 % slower; 3 spills)
+#endif
+#ifndef PD_TFX_TWX_SMEM
+#define PD_TFX_TWX_SMEM 1  // NX-point twiddles staged in smem (0: read through L1)
+#endif
 constexpr int kRS = PD_TFX_S1_RM;
 
 template <int NT, int NX>
@@ -51,20 +57,20 @@ struct Fx {
 // forward stage 2 + x-FFT
 // ---------------------------------------------------------------------------------------------
 template <int NT, int NX>
-__global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_fwd_s2(const double2* __restrict__ Y, long long S,
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2(const double2* __restrict__ Y, long long S,
                                                              long long p_begin, long long Pc,
                                                              double2* __restrict__ Sh,
                                                              const double2* __restrict__ twx) {
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, C = F::C, NTH = F::NTH;
   extern __shared__ double2 sm[];
-  __shared__ double2 s_twx[NX], s_twp[NP];
+  __shared__ double2 s_twx[PD_TFX_TWX_SMEM ? NX : 1], s_twp[NP];
   const int n2 = blockIdx.y, n2p = (N2 - n2) % N2;
   const long long pl0 = (long long)blockIdx.x * NP;  // first pair of this x-row within the chunk
   const long long p0 = p_begin + pl0;
   for (int i = threadIdx.x; i < NX; i += NTH) {
     const double2 w = __ldg(twx + i);
-    s_twx[i] = w;
+    if (PD_TFX_TWX_SMEM) s_twx[i] = w;
     if (!(i & 1)) s_twp[i >> 1] = w;
   }
   // (1) N1-point DFTs over t1 of the sequences c = (set, p); row (n1, set) keeps p contiguous
@@ -111,7 +117,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_fwd_s2(const double2* __r
     const double2 b = sm[pad((2 * n1p + setp) * NP + ((NP - k) & (NP - 1)))];
     const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));     // (a + conj b) / 2
     const double2 O = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));    // (a - conj b) / 2i
-    __stcs(Sh + (long long)n * S + 2 * p0 + kx, cfma(s_twx[kx], O, E));
+    __stcs(Sh + (long long)n * S + 2 * p0 + kx, cfma(PD_TFX_TWX_SMEM ? s_twx[kx] : __ldg(twx + kx), O, E));
   }
 }
 
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_fwd_s2(const double2* __r
 // x-IFFT + inverse stage 1
 // ---------------------------------------------------------------------------------------------
 template <int NT, int NX>
-__global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_inv_s1(const double2* __restrict__ Sh, long long S,
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1(const double2* __restrict__ Sh, long long S,
                                                              long long p_begin, long long Pc,
                                                              double2* __restrict__ W,
                                                              const double2* __restrict__ twx,
@@ -127,13 +133,13 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_inv_s1(const double2* __r
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, C = F::C, NTH = F::NTH;
   extern __shared__ double2 sm[];
-  __shared__ double2 s_twx[NX], s_twp[NP], s_twa[N1], s_twb[N1];
+  __shared__ double2 s_twx[PD_TFX_TWX_SMEM ? NX : 1], s_twp[NP], s_twa[N1], s_twb[N1];
   const int n2 = blockIdx.y, n2p = (N2 - n2) % N2;
   const long long pl0 = (long long)blockIdx.x * NP;
   const long long p0 = p_begin + pl0;
   for (int i = threadIdx.x; i < NX; i += NTH) {
     const double2 w = __ldg(twx + i);
-    s_twx[i] = w;
+    if (PD_TFX_TWX_SMEM) s_twx[i] = w;
     if (!(i & 1)) s_twp[i >> 1] = w;
   }
   if (threadIdx.x < N1) {
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH) tfx_inv_s1(const double2* __r
         x1[r] = __ldcs(q + NP);
       }
     }
-    const double2 wk = s_twx[k];
+    const double2 wk = PD_TFX_TWX_SMEM ? s_twx[k] : __ldg(twx + k);
 #pragma unroll
     for (int r = 0; r < 2 * N1; ++r) {
       const int set = r / N1, n1 = r % N1;
