@@ -51,7 +51,7 @@ template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, double* __restrict__ y, long long n2,
                                                           double* __restrict__ partial, const double* tail_y,
                                                           long long n) {
-  constexpr int NACC = (MODE == 2 || MODE == 3) ? 1 : K;
+  constexpr int NACC = (MODE == 2 || MODE == 3) ? 1 : MODE == 4 ? K + 1 : K;  // mode 4: dots + ||y_new||^2
   // per-block contiguous range of double2 elements
   const long long per = (n2 + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * per, hi = min(n2, lo + per);
@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
     } else if constexpr (MODE != 3) {
 #pragma unroll
       for (int i = 0; i < K; ++i) acc[i] = fma(xv[i].x, yv.x, fma(xv[i].y, yv.y, acc[i]));
+      if constexpr (MODE == 4) acc[NACC - 1] = fma(yv.x, yv.x, fma(yv.y, yv.y, acc[NACC - 1]));
     }
   }
   // odd tail element (n odd): handled by block 0 thread 0
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
       } else if constexpr (MODE != 3) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = fma(X.p[i][t], yv, acc[i]);
+        if constexpr (MODE == 4) acc[NACC - 1] = fma(yv, yv, acc[NACC - 1]);
       }
     }
   }

@@ -711,7 +711,7 @@ pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double*
   phase_begin(c, 6);
   PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st));
   if (mode != 3) {
-    const int kk = mode == 2 ? 1 : k;
+    const int kk = mode == 2 ? 1 : mode == 4 ? k + 1 : k;
     PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), kk, c->dred, c->st));
     phase_end(c, 6);
     if (c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
@@ -867,7 +867,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
   double beta = std::sqrt(rr);
   int its = 0;
   bool conv = beta <= tol * bnorm, breakdown = false;
-  std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m), coef(m + 1), sc(m + 1);
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 2), y(m), coef(m + 1), sc(m + 1);
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
   const double* const* Xp = Xv.data();
   // corner identity path (single GPU, linear operator); PD_GMRES_MATVEC=1 keeps the explicit matvec
@@ -877,6 +877,8 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
                       c->nt >= 2 * gcorner.H && getenv("PD_GMRES_MATVEC") == nullptr;
   const long long hn_len = (long long)gcorner.H * c->S;
   std::vector<double> eh(m + 1);
+  double ww_known = -1.0;                 // ||w||^2 when the second CGS pass is skipped
+  const double kReorthSkip = getenv("PD_GMRES_ALWAYS_CGS2") ? -1.0 : 1e-12;
   double* dhead = nullptr;
   if (corner) {
     if (!c->gm_head) PD_CUDA(c, dalloc(&c->gm_head, (size_t)(2 * c->S + 2)));
@@ -906,17 +908,34 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
           h[i] = (i == j ? 1.0 : 0.0) - sc[i] * sc[j] * eh[i];
           coef[i] = -h[i] * sc[i] / sc[j];
         }
-        coef[j] += 1.0;  // w_raw = X_j + E_H delta - sum (h_i sc_i / sc_j) X_i
-        s = pd_krylov_n(c, 4, Xp, coef.data(), j + 1, 0.0, w, n, h2.data());  // written fresh, dots of the X part
+        coef[j] = sc[j] * sc[j] * eh[j];  // 1 - h_jj without cancellation: w_raw = X_j + E_H delta - sum h_i sc_i/sc_j X_i
+        s = pd_krylov_n(c, 4, Xp, coef.data(), j + 1, 0.0, w, n, h2.data());  // written fresh: dots + ||.||^2
+        if (s != PD_OK) return s;
+        // + E_H delta (delta = -G tail); ||w||^2 updated from the head before/after (head-sized dots)
+        double hb = 0, ha = 0;
+        const double* wv[1] = {w};
+        s = pd_krylov_n(c, 0, wv, nullptr, 1, 0.0, w, hn_len, &hb);
         if (s != PD_OK) return s;
         const double* hx[2] = {w, dhead};
         const double hc[2] = {1.0, -1.0};
-        s = pd_krylov_n(c, 3, hx, hc, 2, 0.0, w, hn_len, nullptr);  // + E_H delta (delta = -G tail)
+        s = pd_krylov_n(c, 3, hx, hc, 2, 0.0, w, hn_len, nullptr);
         if (s != PD_OK) return s;
+        s = pd_krylov_n(c, 0, wv, nullptr, 1, 0.0, w, hn_len, &ha);
+        if (s != PD_OK) return s;
+        const double ww1 = std::max(0.0, h2[j + 1] - hb + ha);
+        double pmax = 0.0;
         for (int i = 0; i <= j; ++i) {
           h2[i] = sc[i] * sc[j] * (h2[i] - eh[i]);
-          coef[i] = -h2[i] * sc[i] / sc[j];
-          h[i] += h2[i];
+          pmax = std::max(pmax, std::fabs(h2[i]));
+        }
+        if (pmax <= kReorthSkip * sc[j] * std::sqrt(ww1)) {
+          // measured projections below 1e-12 of the vector: the second CGS pass would not change it
+          ww_known = ww1;
+        } else {
+          for (int i = 0; i <= j; ++i) {
+            coef[i] = -h2[i] * sc[i] / sc[j];
+            h[i] += h2[i];
+          }
         }
       } else {
         s = pd_stencil_impl(c, nullptr, c->zvec, w, nullptr);
@@ -937,8 +956,13 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
         }
       }
       double ww = 0;
-      s = krylov_impl(c, 2, Xp, coef.data(), j + 1, 1.0, w, &ww);
-      if (s != PD_OK) return s;
+      if (ww_known >= 0.0) {
+        ww = ww_known;
+        ww_known = -1.0;
+      } else {
+        s = krylov_impl(c, 2, Xp, coef.data(), j + 1, 1.0, w, &ww);
+        if (s != PD_OK) return s;
+      }
       const double hn = sc[j] * std::sqrt(ww);
       for (int i = 0; i <= j; ++i) Hs(i, j) = h[i];
       Hs(j + 1, j) = hn;

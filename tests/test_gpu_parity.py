@@ -273,9 +273,11 @@ def test_gmres_corner_identity_equals_matvec_path(name, monkeypatch):
     b = problems.rhs(cfg, u0, v0, f)
     ctx = make_ctx(cfg)
     u1, r1 = ctx.solve_gmres(to_dev(b), tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
+    monkeypatch.setenv("PD_GMRES_ALWAYS_CGS2", "1")  # second CGS pass unconditionally (no measured-skip)
+    u3, r3 = ctx.solve_gmres(to_dev(b), tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
     monkeypatch.setenv("PD_GMRES_MATVEC", "1")
     u2, r2 = ctx.solve_gmres(to_dev(b), tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
-    assert r1.iterations == r2.iterations and r1.converged and r2.converged
-    assert rel(to_host(u1), to_host(u2)) < 1e-10
+    assert r1.iterations == r2.iterations == r3.iterations and r1.converged and r2.converged
+    assert rel(to_host(u1), to_host(u2)) < 1e-10 and rel(to_host(u3), to_host(u2)) < 1e-10
     for a, c in zip(r1.history, r2.history):
         assert abs(a - c) <= 1e-6 * c + 1e-14
