@@ -122,6 +122,8 @@ struct pd_ctx {
     double2* hc = nullptr;    // 1D: [F][H] economical Step (a) coefficients
     double2* ow = nullptr;    // 1D: [F][H] Step (c) weights of the last H rows (with multiplicity)
     double* part = nullptr;   // 1D: [G][H][S] per-CTA partial sums
+    double* acc = nullptr;    // [H][Sg] per-shard tail accumulation (virtual ranks)
+    pd_stencil gsten{};       // stencil of the GLOBAL grid (heads and tails are replicated on every rank)
     double2* tau = nullptr;   // 2D: [N][N] transfer function
     double2* work = nullptr;  // 2D: [N][N] complex slab
     std::vector<double*> scr;  // head-sized scratch vectors
@@ -165,8 +167,9 @@ pd_status pd_dist_build_rhs(pd_ctx* c, const double* u0, const double* v0, const
 // paradiag.cpp helpers used by dist.cpp and tailform.cpp
 pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate);
 pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2);
+// reduced values are all-reduced across NCCL ranks unless global_sum is false (vectors replicated on every rank)
 pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a, double* y,
-                      long long n, double* host_out);
+                      long long n, double* host_out, bool global_sum = true);
 extern "C" void pd_report_push(pd_report* rep, double v);
 void pd_tail_free(pd_ctx* c);
 void pd_corner_coefs(const pd_ctx* c, pd_tail_g* gc);

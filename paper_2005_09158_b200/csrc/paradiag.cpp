@@ -707,14 +707,14 @@ pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* o
 // Krylov sweep (blas1.cu) over the local vector; the k (or 1) reduced values all-reduced across ranks and
 // copied to host_out (syncs) unless host_out == NULL (mode 3)
 pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a, double* y,
-                      long long n, double* host_out) {
+                      long long n, double* host_out, bool global_sum) {
   phase_begin(c, 6);
   PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st));
   if (mode != 3) {
     const int kk = mode == 2 ? 1 : mode == 4 ? k + 1 : k;
     PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), kk, c->dred, c->st));
     phase_end(c, 6);
-    if (c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
+    if (global_sum && c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
       return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
     PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, kk * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     PD_CUDA(c, cudaStreamSynchronize(c->st));

@@ -10,7 +10,11 @@
 //   Step (b) for every frequency and only the last H rows of Step (c) - tridiag.cu tail1d_kernel in 1D, the
 //   transfer function tau in 2D (tail.cu).  Per iteration the work is O(H S) memory traffic plus the per-
 //   frequency solves (1D) instead of three full passes over Nt S dofs.
-// Single-GPU contexts only in this version (the sharded variant needs an H*S all-reduce).
+// Sharded contexts (SURVEY 8(f) NEXT-1 at P > 1): heads and tails (H x S_global values) are replicated on every
+// rank, so all O(H S) work is redundant and reduction-free; the 1D tail map splits the frequency range over the
+// ranks and sums with one H S all-reduce (instead of the two all-to-alls of a full apply), the 2D tail map (a
+// slab FFT filter, microseconds) runs on every rank; only the full applies at start and exit are distributed.
+// The virtual-rank executor runs the same per-shard frequency split on one GPU.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -27,7 +31,7 @@ constexpr int kScr = 10;  // head-sized scratch vectors
 cudaError_t dalloc_d(double** p, size_t n) { return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 2) * sizeof(double)); }
 cudaError_t dalloc_c(double2** p, size_t n) { return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(double2)); }
 
-long long hs(const pd_ctx* c) { return (long long)c->tail.H * c->S; }
+long long hs(const pd_ctx* c) { return (long long)c->tail.H * c->Sg; }   // replicated head / tail size
 
 }  // namespace
 
@@ -64,13 +68,19 @@ namespace {
 pd_status tail_setup(pd_ctx* c) {
   auto& T = c->tail;
   if (T.ready) return PD_OK;
-  if (c->dist_mode != 0) return fail(c, PD_EINVAL, "tail form: single-GPU contexts only");
   if (c->g.op == PD_WAVE2D_DIRICHLET) return fail(c, PD_EINVAL, "tail form: not built for the 2D Dirichlet operator");
   const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
   if (c->nt < 2 * H) return fail(c, PD_EINVAL, "tail form needs Nt >= %d", 2 * H);
   const int nt = c->nt, F = c->F;
-  const double dt = c->dt, al = c->alpha;
+  const double al = c->alpha;
   pd_corner_coefs(c, &T.gc);
+  // global-grid stencil for the head-from-tail product on the replicated tails
+  T.gsten = c->sten;
+  if (c->dist_mode == 1) {
+    T.gsten.nx = c->g.nx;
+    T.gsten.ny = c->g.ny;
+  }
+  T.gsten.hlo = T.gsten.hhi = nullptr;
   // economical Step (a) coefficients and last-H-row Step (c) weights (long double, closed form)
   typedef std::complex<long double> cld;
   const long double pi = 3.141592653589793238462643383279502884L;
@@ -91,7 +101,7 @@ pd_status tail_setup(pd_ctx* c) {
     const cld wv = cld(ow[(size_t)n * H].x, ow[(size_t)n * H].y) * cld(hc[(size_t)n * H].x, hc[(size_t)n * H].y);
     w2[n] = make_double2((double)wv.real(), (double)wv.imag());
   }
-  const long long S = c->S;
+  const long long Sg = c->Sg;
   if (c->g.op == PD_ADE2D_PERIODIC) {
     const int N = c->g.nx;
     double2* wd = nullptr;
@@ -108,10 +118,11 @@ pd_status tail_setup(pd_ctx* c) {
     PD_CUDA(c, cudaMemcpy(T.hc, hc.data(), hc.size() * sizeof(double2), cudaMemcpyHostToDevice));
     PD_CUDA(c, cudaMemcpy(T.ow, ow.data(), ow.size() * sizeof(double2), cudaMemcpyHostToDevice));
     T.G = std::min(F, 4 * 148);
-    PD_CUDA(c, dalloc_d(&T.part, (size_t)T.G * H * S));
+    PD_CUDA(c, dalloc_d(&T.part, (size_t)T.G * H * Sg));
+    if (c->dist_mode == 2) PD_CUDA(c, dalloc_d(&T.acc, (size_t)H * Sg));
   }
   T.scr.assign(kScr, nullptr);
-  for (auto& p : T.scr) PD_CUDA(c, dalloc_d(&p, (size_t)H * S));
+  for (auto& p : T.scr) PD_CUDA(c, dalloc_d(&p, (size_t)H * Sg));
   PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&T.flag), sizeof(int)));
   PD_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&T.hflag), sizeof(int)));
   T.H = H;
@@ -119,51 +130,105 @@ pd_status tail_setup(pd_ctx* c) {
   return PD_OK;
 }
 
-// out = T(g): last H blocks of P^{-1}(E_H g)   (g, out: [H][S], out must not alias g)
+pd_status allreduce(pd_ctx* c, double* d, long long n) {
+  if (c->dist_mode != 1) return PD_OK;
+  if (pd_comm_allreduce_sum(c->comm, d, (int)n) != 0) return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
+  return PD_OK;
+}
+
+// full [H][Sg] (replicated) <- the H blocks starting at `rows` of a local [Nt][S] vector
+pd_status gather_full(pd_ctx* c, const double* rows, double* full) {
+  const int H = c->tail.H;
+  if (c->dist_mode != 1) {
+    PD_CUDA(c, cudaMemcpyAsync(full, rows, sizeof(double) * H * c->Sg, cudaMemcpyDeviceToDevice, c->st));
+    return PD_OK;
+  }
+  PD_CUDA(c, cudaMemsetAsync(full, 0, sizeof(double) * H * c->Sg, c->st));
+  for (int t = 0; t < H; ++t)
+    PD_CUDA(c, cudaMemcpyAsync(full + (long long)t * c->Sg + c->off, rows + (long long)t * c->S, sizeof(double) * c->S,
+                               cudaMemcpyDeviceToDevice, c->st));
+  return allreduce(c, full, (long long)H * c->Sg);
+}
+
+// the H blocks starting at `rows` of a local vector <- this rank's part of full [H][Sg]
+pd_status local_of(pd_ctx* c, const double* full, double* rows) {
+  const int H = c->tail.H;
+  for (int t = 0; t < H; ++t)
+    PD_CUDA(c, cudaMemcpyAsync(rows + (long long)t * c->S, full + (long long)t * c->Sg + (c->dist_mode == 1 ? c->off : 0),
+                               sizeof(double) * c->S, cudaMemcpyDeviceToDevice, c->st));
+  return PD_OK;
+}
+
+pd_status comb(pd_ctx* c, std::vector<const double*> X, std::vector<double> coef, double* y, long long n) {
+  return pd_krylov_n(c, 3, X.data(), coef.data(), (int)X.size(), 0.0, y, n, nullptr, false);
+}
+
+// out = T(g): last H blocks of P^{-1}(E_H g)   (g, out: replicated [H][Sg], out must not alias g)
 pd_status tail_map(pd_ctx* c, const double* g, double* out) {
   auto& T = c->tail;
-  const long long S = c->S;
-  if (c->g.op == PD_ADE2D_PERIODIC) {
-    PD_LAUNCH(c, pd_launch_r2c(g, T.work, S, c->st));
+  const long long Sg = c->Sg, Hn = (long long)T.H * Sg;
+  if (c->g.op == PD_ADE2D_PERIODIC) {  // every rank: one slab FFT filter of the whole head
+    PD_LAUNCH(c, pd_launch_r2c(g, T.work, Sg, c->st));
     PD_CUDA(c, pd_launch_slab2d_filter(T.work, c->g.nx, T.tau, c->tw_s, c->st));
     c->launches += 3;
-    PD_LAUNCH(c, pd_launch_take_real(T.work, out, S, c->st));
-  } else {
-    PD_LAUNCH(c, pd_launch_tail1d(g, T.part, T.G, c->g.nx, c->F, T.H, c->tri, T.hc, T.ow, c->st));
-    PD_LAUNCH(c, pd_launch_reduce_rows(T.part, T.G, (long long)T.H * S, out, c->st));
+    PD_LAUNCH(c, pd_launch_take_real(T.work, out, Sg, c->st));
+    return PD_OK;
+  }
+  auto range = [&](int f0, int fc, double* dst) -> pd_status {
+    const int G = std::max(1, std::min(fc, T.G));
+    PD_LAUNCH(c, pd_launch_tail1d(g, T.part, G, c->g.nx, fc, T.H, c->tri + f0, T.hc + (long long)f0 * T.H,
+                                  T.ow + (long long)f0 * T.H, c->st));
+    PD_LAUNCH(c, pd_launch_reduce_rows(T.part, G, Hn, dst, c->st));
+    return PD_OK;
+  };
+  if (c->dist_mode == 0) return range(0, c->F, out);
+  if (c->dist_mode == 1) {  // this rank's frequencies, summed over the ranks
+    pd_status s = range(c->plan.f_off[c->rank], c->plan.f_cnt[c->rank], out);
+    return s != PD_OK ? s : allreduce(c, out, Hn);
+  }
+  // virtual ranks: the same split, summed on the device in shard order
+  for (size_t i = 0; i < c->shards.size(); ++i) {
+    const int f0 = c->plan.f_off[i], fc = c->plan.f_cnt[i];
+    if (fc == 0) continue;
+    pd_status s = range(f0, fc, i == 0 ? out : T.acc);
+    if (s != PD_OK) return s;
+    if (i > 0) {
+      s = comb(c, {out, T.acc}, {1.0, 1.0}, out, Hn);
+      if (s != PD_OK) return s;
+    }
   }
   return PD_OK;
 }
 
 pd_status head_G(pd_ctx* c, const double* tail, double* head) {
-  PD_LAUNCH(c, pd_launch_head_G(c->sten, c->tail.gc, tail, head, c->S, c->st));
+  PD_LAUNCH(c, pd_launch_head_G(c->tail.gsten, c->tail.gc, tail, head, c->Sg, c->st));
   return PD_OK;
 }
 
-// true if any of x[0..n) is non-zero (syncs)
+// true if any of x[0..n) is non-zero on any rank (syncs)
 pd_status any_nonzero(pd_ctx* c, const double* x, long long n, bool* out) {
   auto& T = c->tail;
   PD_CUDA(c, cudaMemsetAsync(T.flag, 0, sizeof(int), c->st));
   PD_LAUNCH(c, pd_launch_any_nonzero(x, n, T.flag, c->st));
   PD_CUDA(c, cudaMemcpyAsync(T.hflag, T.flag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   PD_CUDA(c, cudaStreamSynchronize(c->st));
-  *out = *T.hflag != 0;
+  double v = *T.hflag != 0 ? 1.0 : 0.0;
+  if (c->dist_mode == 1) {
+    c->hred[0] = v;
+    PD_CUDA(c, cudaMemcpyAsync(c->dred, c->hred, sizeof(double), cudaMemcpyHostToDevice, c->st));
+    pd_status s = allreduce(c, c->dred, 1);
+    if (s != PD_OK) return s;
+    PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    PD_CUDA(c, cudaStreamSynchronize(c->st));
+    v = c->hred[0];
+  }
+  *out = v != 0.0;
   return PD_OK;
 }
 
+// dots of replicated vectors (no cross-rank sum)
 pd_status dots(pd_ctx* c, std::vector<const double*> X, const double* y, long long n, double* out) {
-  return pd_krylov_n(c, 0, X.data(), nullptr, (int)X.size(), 0.0, const_cast<double*>(y), n, out);
-}
-// y = sum c_i X_i (X may contain y)
-pd_status comb(pd_ctx* c, std::vector<const double*> X, std::vector<double> coef, double* y, long long n) {
-  return pd_krylov_n(c, 3, X.data(), coef.data(), (int)X.size(), 0.0, y, n, nullptr);
-}
-
-pd_status copy_tail(pd_ctx* c, const double* u, double* t) {
-  const long long S = c->S;
-  PD_CUDA(c, cudaMemcpyAsync(t, u + (long long)(c->nt - c->tail.H) * S, sizeof(double) * hs(c), cudaMemcpyDeviceToDevice,
-                             c->st));
-  return PD_OK;
+  return pd_krylov_n(c, 0, X.data(), nullptr, (int)X.size(), 0.0, const_cast<double*>(y), n, out, false);
 }
 
 pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {
@@ -182,7 +247,7 @@ pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {
 
 void pd_tail_free(pd_ctx* c) {
   auto& T = c->tail;
-  for (void* p : {(void*)T.hc, (void*)T.ow, (void*)T.part, (void*)T.tau, (void*)T.work, (void*)T.flag})
+  for (void* p : {(void*)T.hc, (void*)T.ow, (void*)T.part, (void*)T.tau, (void*)T.work, (void*)T.flag, (void*)T.acc})
     if (p) cudaFree(p);
   for (double* p : T.scr) cudaFree(p);
   for (double* p : T.Vh) cudaFree(p);
@@ -195,7 +260,12 @@ extern "C" {
 pd_status pd_tail_map(pd_ctx* c, const double* head, double* tail) {
   if (!c || !head || !tail) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
   PD_TRY(tail_setup(c));
-  return tail_map(c, head, tail);
+  if (c->dist_mode != 1) return tail_map(c, head, tail);
+  // NCCL ranks: local head slab in, local tail slab out
+  auto& T = c->tail;
+  PD_TRY(gather_full(c, head, T.scr[8]));
+  PD_TRY(tail_map(c, T.scr[8], T.scr[9]));
+  return local_of(c, T.scr[9], tail);
 }
 
 pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double tol, int maxit, pd_report* rep) {
@@ -205,7 +275,7 @@ pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double
   const auto t0 = std::chrono::steady_clock::now();
   if (rep) rep->history_len = 0;
   auto& T = c->tail;
-  const long long n = (long long)c->nt * c->S, Hn = hs(c);
+  const long long n = (long long)c->nt * c->S, Hn = hs(c), Hl = (long long)T.H * c->S;
   double bb = 0;
   PD_TRY(pd_krylov_n(c, 0, &b, nullptr, 1, 0.0, const_cast<double*>(b), n, &bb));
   const double bnorm = std::sqrt(bb);
@@ -215,15 +285,17 @@ pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double
   double rel = std::sqrt(rr) / bnorm;
   int k = 0;
   if (rel > tol && maxit > 0) {
-    double *tp = T.scr[0], *tc = T.scr[1], *yt = T.scr[2], *hd = T.scr[3], *dd = T.scr[4];
-    PD_TRY(copy_tail(c, u, tp));  // t^0
+    double *tp = T.scr[0], *tc = T.scr[1], *yt = T.scr[2], *hd = T.scr[3], *dd = T.scr[4], *bh = T.scr[5];
+    const long long tail_off = (long long)(c->nt - T.H) * c->S;
+    PD_TRY(gather_full(c, u + tail_off, tp));  // t^0
     bool nonhead = true;
-    PD_TRY(any_nonzero(c, b + Hn, n - Hn, &nonhead));
+    PD_TRY(any_nonzero(c, b + Hl, n - Hl, &nonhead));
     if (nonhead) {
       PD_TRY(pd_apply_impl(c, b, u, 0));  // u = y = P^{-1} b
-      PD_TRY(copy_tail(c, u, yt));
+      PD_TRY(gather_full(c, u + tail_off, yt));
     } else {
-      PD_TRY(tail_map(c, b, yt));  // b supported on the head: tail(P^{-1} b) = T(b_head)
+      PD_TRY(gather_full(c, b, bh));
+      PD_TRY(tail_map(c, bh, yt));  // b supported on the head: tail(P^{-1} b) = T(b_head)
     }
     for (;;) {
       PD_TRY(head_G(c, tp, hd));
@@ -231,7 +303,7 @@ pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double
       PD_TRY(comb(c, {tc, yt}, {1.0, 1.0}, tc, Hn));  // t^{k+1} = y_tail + T(G t^k)
       ++k;
       PD_TRY(comb(c, {tc, tp}, {1.0, -1.0}, dd, Hn));
-      PD_TRY(head_G(c, dd, hd));                      // r^{k+1} = E_H G (t^{k+1} - t^k)
+      PD_TRY(head_G(c, dd, hd));  // r^{k+1} = E_H G (t^{k+1} - t^k)
       double h2 = 0;
       PD_TRY(dots(c, {hd}, hd, Hn, &h2));
       rel = std::sqrt(h2) / bnorm;
@@ -243,10 +315,11 @@ pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double
     PD_TRY(head_G(c, tp, hd));
     PD_CUDA(c, cudaMemsetAsync(c->rvec, 0, sizeof(double) * n, c->st));
     if (nonhead) {
-      PD_CUDA(c, cudaMemcpyAsync(c->rvec, hd, sizeof(double) * Hn, cudaMemcpyDeviceToDevice, c->st));
+      PD_TRY(local_of(c, hd, c->rvec));
       PD_TRY(pd_apply_impl(c, c->rvec, u, 1));  // u = y + P^{-1}(E_H G t^{k-1})
     } else {
-      PD_TRY(comb(c, {b, hd}, {1.0, 1.0}, c->rvec, Hn));
+      PD_TRY(comb(c, {bh, hd}, {1.0, 1.0}, hd, Hn));
+      PD_TRY(local_of(c, hd, c->rvec));
       PD_TRY(pd_apply_impl(c, c->rvec, u, 0));
     }
   }
@@ -267,7 +340,8 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
   const auto t0 = std::chrono::steady_clock::now();
   if (rep) rep->history_len = 0;
   auto& T = c->tail;
-  const long long n = (long long)c->nt * c->S, Hn = hs(c);
+  const long long n = (long long)c->nt * c->S, Hn = hs(c), Hl = (long long)T.H * c->S;
+  const long long tail_off = (long long)(c->nt - T.H) * c->S;
   if ((int)T.Vh.size() < m + 1) {
     for (double* p : T.Vh) cudaFree(p);
     T.Vh.assign(m + 1, nullptr);
@@ -283,16 +357,16 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
   double beta = std::sqrt(rr);
   int its = 0;
   bool conv = beta <= tol * bnorm, breakdown = false;
-  double *q0 = T.scr[0], *tq = T.scr[1], *gt = T.scr[2], *w = T.scr[3], *ch = T.scr[4];
-  const double* r0h = c->rvec;  // head of the anchor
+  double *q0 = T.scr[0], *tq = T.scr[1], *gt = T.scr[2], *w = T.scr[3], *ch = T.scr[4], *r0h = T.scr[5];
   std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), y(m), A(m + 1), Sd(m + 1), d(m + 2), d2(m + 2);
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
   while (!conv && its < maxit) {
     bool nonhead = true;
-    PD_TRY(any_nonzero(c, c->rvec + Hn, n - Hn, &nonhead));
+    PD_TRY(gather_full(c, c->rvec, r0h));  // replicated head of the anchor
+    PD_TRY(any_nonzero(c, c->rvec + Hl, n - Hl, &nonhead));
     if (nonhead) {
       PD_TRY(pd_apply_impl(c, c->rvec, c->zvec, 0));  // q0 = G tail(P^{-1} r0)
-      PD_TRY(copy_tail(c, c->zvec, tq));
+      PD_TRY(gather_full(c, c->zvec + tail_off, tq));
       PD_TRY(head_G(c, tq, q0));
       A[0] = 1.0 / beta;
       PD_CUDA(c, cudaMemsetAsync(T.Vh[0], 0, sizeof(double) * Hn, c->st));
@@ -332,7 +406,7 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
         }
         wa -= da;
         // w <- w - sum h_i h_i-vectors; partial dots of the updated w with X (next pass / norm)
-        PD_TRY(pd_krylov_n(c, 1, X.data(), coef.data(), j + 2, 1.0, w, Hn, d.data()));
+        PD_TRY(pd_krylov_n(c, 1, X.data(), coef.data(), j + 2, 1.0, w, Hn, d.data(), false));
       }
       double ww = 0;
       PD_TRY(dots(c, {w}, w, Hn, &ww));
@@ -372,9 +446,10 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
     for (int i = 0; i < kk; ++i) ca += y[i] * A[i];
     std::vector<const double*> Xc(T.Vh.begin(), T.Vh.begin() + kk);
     PD_TRY(comb(c, Xc, std::vector<double>(y.begin(), y.begin() + kk), ch, Hn));
-    // u += P^{-1}(ca r0 + E_H ch): the anchor buffer becomes the right-hand side
+    // u += P^{-1}(ca r0 + E_H ch): the anchor buffer becomes the right-hand side (this rank's part of ch)
     PD_LAUNCH(c, pd_launch_axpby(c->rvec, c->rvec, ca, 0.0, n, c->st));
-    PD_TRY(comb(c, {c->rvec, ch}, {1.0, 1.0}, c->rvec, Hn));
+    PD_TRY(local_of(c, ch, gt));
+    PD_TRY(comb(c, {c->rvec, gt}, {1.0, 1.0}, c->rvec, Hl));
     PD_TRY(pd_apply_impl(c, c->rvec, u, 1));
     PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // true residual; the next cycle's anchor
     beta = std::sqrt(rr);

@@ -175,3 +175,50 @@ def test_two_rank_plan_matches_oracle(cfg, P):
         assert p.exitcode == 0
     e1, e2 = q.get(timeout=10)
     assert e1 < 1e-12 and e2 < 1e-13
+
+
+def _tail_worker(rank, P, port, cfg, out_q):
+    """Sharded tail map (tailform.cpp, NCCL mode): every rank holds the replicated head, solves the shifted systems
+    of its plan's half-spectrum frequencies [f_off, f_off + f_cnt), weights the last H rows of Step (c) with the
+    half-spectrum multiplicities, and one all-reduce sums the partial tails."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        from paper_2005_09158_b200 import partition
+        from oracle import tail
+        _, _, f_off, f_cnt = partition(OPS[cfg.op], cfg.nx, cfg.ny, cfg.nt, P)
+        nt, H = cfg.nt, tail.head_blocks(cfg)
+        g = np.random.default_rng(21).standard_normal((H, cfg.S))
+        gam = spectral.gamma(nt, cfg.alpha)
+        lam1, lam2 = spectral.spectra(cfg)
+        fs = np.arange(f_off[rank], f_off[rank] + f_cnt[rank])
+        S1 = sum((gam[t] * np.exp(-2j * np.pi * fs * t / nt))[:, None] * g[t][None, :] for t in range(H))
+        S2 = spectral.step_b(cfg, S1, lam1[fs], lam2[fs])
+        mult = np.where((fs == 0) | (2 * fs == nt), 1.0, 2.0)
+        part = np.zeros((H, cfg.S))
+        for a in range(H):
+            t = nt - H + a
+            w = mult * np.exp(2j * np.pi * fs * t / nt) / nt / gam[t]
+            part[a] = (w[:, None] * S2).real.sum(axis=0)
+        tt = torch.from_numpy(part)
+        dist.all_reduce(tt)
+        if rank == 0:
+            ref = tail.tail_map(cfg, g)
+            out_q.put(float(np.linalg.norm(tt.numpy() - ref) / np.linalg.norm(ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,P", [(W.CONFIGS[1].scaled(nx=31, nt=16), 2), (W.CONFIGS[2].scaled(nx=30, nt=16), 3)])
+def test_sharded_tail_map_frequency_split(cfg, P):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tail_worker, args=(r, P, port, cfg, q)) for r in range(P)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) < 1e-11

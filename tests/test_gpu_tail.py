@@ -133,10 +133,35 @@ def test_tail_cfg2_matches_sequential():
     assert rel(to_host(u), seq) < SOLVE_TOL
 
 
-def test_tail_rejects_sharded():
-    cfg = W.CONFIGS[0]
-    ctx = make_ctx(cfg, rank=-1, size=2)
+@pytest.mark.parametrize("name,P", [("cfg1", 3), ("cfg2", 2), ("cfg3", 4), ("cfg0", 2)])
+def test_tail_sharded_virtual_ranks(name, P):
+    """Sharded tail form on P virtual ranks (replicated heads, per-shard frequency split of the 1D tail map summed
+    over the shards, distributed applies at start and exit): same counts and solution as the oracle."""
+    cfg = W.BY_NAME[name]
+    if name == "cfg2":
+        cfg = cfg.scaled(nt=1024)
+    ctx = make_ctx(cfg, rank=-1, size=P)
+    b_dev, b = _rhs(ctx, cfg)
+    g = np.random.default_rng(P).standard_normal((ctx.head_blocks, cfg.S))
+    t_ref = tail.tail_map(cfg, g)
+    v = np.zeros((cfg.nt, cfg.S))
+    v[: ctx.head_blocks] = g
+    scale = np.linalg.norm(spectral.apply_precond(cfg, v))
+    assert np.linalg.norm(to_host(ctx.tail_map(to_dev(g))) - t_ref) <= 1e-10 * max(scale, 1.0)
+    if cfg.solver == "stationary":
+        u, rep = ctx.solve_stationary_tail(b_dev, tol=cfg.tol, maxit=cfg.maxit)
+        u_ref, rep_ref = solvers.solve_stationary(cfg, b)
+    else:
+        u, rep = ctx.solve_gmres_tail(b_dev, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
+        u_ref, rep_ref = solvers.solve_gmres(cfg, b)
+    assert rep.converged and rep.iterations == rep_ref.iterations
+    assert rel(to_host(u), u_ref) < SOLVE_TOL
+
+
+def test_tail_rejects_2d_dirichlet():
+    cfg = W.t4a_config(32)
+    ctx = make_ctx(cfg)
     from paper_2005_09158_b200 import ParaDiagError
     with pytest.raises(ParaDiagError):
-        ctx.tail_map(to_dev(np.zeros((1, cfg.S))))
+        ctx.tail_map(to_dev(np.zeros((2, cfg.S))))
     # (Nt >= 2H is already required by pd_setup: Nt >= 2 for the theta-method, >= 4 for leapfrog)
