@@ -343,28 +343,35 @@ PD_D double2 warp_affine_scan(double2 e, double2 M, double2* inc_last) {
   return vl == 0 ? czero() : ex;
 }
 
+#ifndef PD_YTRI_C
+#define PD_YTRI_C 8  // columns (= warps) per CTA
+#endif
+#ifndef PD_YTRI_MINB
+#define PD_YTRI_MINB 0  // 0: by N (3 / 2 / 1)
+#endif
+constexpr int kYC = PD_YTRI_C;
 template <int N>
-__global__ void __launch_bounds__(256, N <= 256 ? 3 : N <= 512 ? 2 : 1) slab_ytri_kernel(double2* __restrict__ Sh, int slab0,
+__global__ void __launch_bounds__(32 * kYC, PD_YTRI_MINB ? PD_YTRI_MINB : (N <= 256 ? 3 : N <= 512 ? 2 : 1)) slab_ytri_kernel(double2* __restrict__ Sh, int slab0,
                                                                           int fglob0,
                                                                           const pd_ytri_coef* __restrict__ coef,
                                                                           double scale) {
   constexpr int L = N / 32, CS = N + 33;
   extern __shared__ double2 sm[];
   const int n = slab0 + blockIdx.y;
-  const int c0 = blockIdx.x * 8;
+  const int c0 = blockIdx.x * kYC;
   double2* slab = Sh + (long long)n * N * N + c0;
   {
-    // all N*8/256 loads of a thread in flight before the first smem store
-    constexpr int PT = N * 8 / 256;
+    // all N/32 loads of a thread in flight before the first smem store
+    constexpr int PT = N / 32;
     double2 v[PT];
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
-      const int i = threadIdx.x + k * 256, r = i >> 3, c = i & 7;
+      const int i = threadIdx.x + k * 32 * kYC, r = i / kYC, c = i % kYC;
       v[k] = __ldcs(slab + (long long)r * N + c);
     }
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
-      const int i = threadIdx.x + k * 256, r = i >> 3, c = i & 7;
+      const int i = threadIdx.x + k * 32 * kYC, r = i / kYC, c = i % kYC;
       sm[c * CS + r + r / L] = v[k];
     }
   }
@@ -411,8 +418,8 @@ __global__ void __launch_bounds__(256, N <= 256 ? 3 : N <= 512 ? 2 : 1) slab_ytr
   for (int j = 0; j < L; ++j) col[j] = d[j];
   __syncthreads();
 #pragma unroll 8
-  for (int i = threadIdx.x; i < N * 8; i += 256) {
-    const int r = i >> 3, c = i & 7;
+  for (int i = threadIdx.x; i < N * kYC; i += 32 * kYC) {
+    const int r = i / kYC, c = i % kYC;
     __stcs(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
   }
 }
@@ -421,7 +428,7 @@ template <int N>
 cudaError_t ytri_n(double2* Sh, int nfreq, int f0g, const pd_ytri_coef* coef, double scale, const double2* tw,
                    int chunk, int rows, cudaStream_t st, int* launches) {
   using T = SlabCfg<N>;
-  const int smem = 8 * (N + 33) * (int)sizeof(double2), smr = smem_bytes<N>();
+  const int smem = kYC * (N + 33) * (int)sizeof(double2), smr = smem_bytes<N>();
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(slab_ytri_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -438,7 +445,7 @@ cudaError_t ytri_n(double2* Sh, int nfreq, int f0g, const pd_ytri_coef* coef, do
     double2* base = Sh + (long long)s0 * N * N;
     const unsigned row_ctas = (unsigned)(ns * (N / T::C));
     if (rows) slab_rows_kernel<N, false><<<row_ctas, T::NTH, smr, st>>>(base, tw);
-    slab_ytri_kernel<N><<<dim3(N / 8, ns), 256, smem, st>>>(Sh, s0, f0g + s0, coef, scale);
+    slab_ytri_kernel<N><<<dim3(N / kYC, ns), 32 * kYC, smem, st>>>(Sh, s0, f0g + s0, coef, scale);
     if (rows) slab_rows_kernel<N, true><<<row_ctas, T::NTH, smr, st>>>(base, tw);
     nl += rows ? 3 : 1;
   }
