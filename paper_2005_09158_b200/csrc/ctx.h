@@ -123,6 +123,7 @@ struct pd_ctx {
     double2* ow = nullptr;    // 1D: [F][H] Step (c) weights of the last H rows (with multiplicity)
     double* part = nullptr;   // 1D: [G][H][S] per-CTA partial sums
     double* acc = nullptr;    // [H][Sg] per-shard tail accumulation (virtual ranks)
+    double2* gx = nullptr;    // [H][Sg] complex head for the head-only apply
     pd_stencil gsten{};       // stencil of the GLOBAL grid (heads and tails are replicated on every rank)
     double2* tau = nullptr;   // 2D: [N][N] transfer function
     double2* work = nullptr;  // 2D: [N][N] complex slab

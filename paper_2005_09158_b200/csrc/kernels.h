@@ -89,6 +89,8 @@ int pd_slab2d_chunk(int n, int nfreq);
 // chunk = slabs per L2-resident chunk; *launches = kernels launched
 // one N x N complex slab in place: 2D FFT, multiply by tab[ky*N + kx] / N^2, inverse 2D FFT (tail map, tail.cu)
 cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, const double2* tw, cudaStream_t st);
+// nrows (multiple of 8) contiguous complex rows of length n: in-place FFT along the row (inv: inverse), unnormalised
+cudaError_t pd_launch_slab2d_rows(double2* base, int n, long long nrows, int inv, const double2* tw, cudaStream_t st);
 cudaError_t pd_launch_slab2d(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                              const double* sx, const double* sn, pd_slab_params prm, const double2* tw,
                              int chunk, int cols_only, cudaStream_t st, int* launches);
@@ -146,6 +148,9 @@ cudaError_t pd_launch_tau2d(double2* tau, int n, int nfreq, const double2* lam1,
                             const double* sx, const double* sn, pd_slab_params prm, cudaStream_t st);
 cudaError_t pd_launch_r2c(const double* g, double2* z, long long n, cudaStream_t st);
 cudaError_t pd_launch_take_real(const double2* z, double* out, long long n, cudaStream_t st);
+// Sh[n][x] = sum_{t<H} hc[n][t] gx[t][x] for n < F (Step (a) of a head-only vector)
+cudaError_t pd_launch_head_broadcast(double2* Sh, int F, long long S, int H, const double2* hc, const double2* gx,
+                                     cudaStream_t st);
 // *flag = 1 if any x[i] != 0 (i < n), else unchanged (caller zeroes it)
 cudaError_t pd_launch_any_nonzero(const double* x, long long n, int* flag, cudaStream_t st);
 

@@ -476,6 +476,35 @@ cudaError_t filter_n(double2* slab, const double2* tab, const double2* tw, cudaS
 
 }  // namespace
 
+template <int N>
+cudaError_t rows_n(double2* base, long long nrows, int inv, const double2* tw, cudaStream_t st) {
+  using T = SlabCfg<N>;
+  const int smem = smem_bytes<N>();
+  cudaError_t e = cudaFuncSetAttribute(slab_rows_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const unsigned ctas = (unsigned)(nrows / T::C);
+  if (inv)
+    slab_rows_kernel<N, true><<<ctas, T::NTH, smem, st>>>(base, tw);
+  else
+    slab_rows_kernel<N, false><<<ctas, T::NTH, smem, st>>>(base, tw);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_slab2d_rows(double2* base, int n, long long nrows, int inv, const double2* tw, cudaStream_t st) {
+  if (nrows % kBatch) return cudaErrorInvalidValue;
+  switch (n) {
+    case 16: return rows_n<16>(base, nrows, inv, tw, st);
+    case 32: return rows_n<32>(base, nrows, inv, tw, st);
+    case 64: return rows_n<64>(base, nrows, inv, tw, st);
+    case 128: return rows_n<128>(base, nrows, inv, tw, st);
+    case 256: return rows_n<256>(base, nrows, inv, tw, st);
+    case 512: return rows_n<512>(base, nrows, inv, tw, st);
+    case 1024: return rows_n<1024>(base, nrows, inv, tw, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, const double2* tw, cudaStream_t st) {
   switch (n) {
     case 16: return filter_n<16>(slab, tab, tw, st);

@@ -78,6 +78,20 @@ __global__ void take_real_kernel(const double2* __restrict__ z, double* __restri
     out[i] = z[i].x;
 }
 
+// Step (a) of a head-only vector E_H g: S1_n = sum_{t<H} hc[n][t] gx_t (economical Step (a), P:l.928-931), written
+// for every frequency of the half spectrum (gx: the head as complex, x-transformed in the fused 2D layout)
+__global__ void head_broadcast_kernel(double2* __restrict__ Sh, int F, long long S, int H, const double2* __restrict__ hc,
+                                      const double2* __restrict__ gx) {
+  const long long total = (long long)F * S;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / S);
+    const long long x = i - (long long)n * S;
+    double2 v = cmul(__ldg(hc + (long long)n * H), gx[x]);
+    if (H == 2) v = cfma(__ldg(hc + (long long)n * H + 1), gx[S + x], v);
+    __stcs(Sh + i, v);
+  }
+}
+
 __global__ void any_nonzero_kernel(const double* __restrict__ x, long long n, int* flag) {
   bool nz = false;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -123,5 +137,11 @@ cudaError_t pd_launch_take_real(const double2* z, double* out, long long n, cuda
 cudaError_t pd_launch_any_nonzero(const double* x, long long n, int* flag, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   any_nonzero_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_head_broadcast(double2* Sh, int F, long long S, int H, const double2* hc, const double2* gx,
+                                     cudaStream_t st) {
+  head_broadcast_kernel<<<148 * 8, 256, 0, st>>>(Sh, F, S, H, hc, gx);
   return cudaGetLastError();
 }

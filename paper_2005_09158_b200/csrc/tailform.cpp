@@ -113,14 +113,15 @@ pd_status tail_setup(pd_ctx* c) {
     PD_CUDA(c, cudaStreamSynchronize(c->st));
     cudaFree(wd);
   } else {
-    PD_CUDA(c, dalloc_c(&T.hc, (size_t)F * H));
     PD_CUDA(c, dalloc_c(&T.ow, (size_t)F * H));
-    PD_CUDA(c, cudaMemcpy(T.hc, hc.data(), hc.size() * sizeof(double2), cudaMemcpyHostToDevice));
     PD_CUDA(c, cudaMemcpy(T.ow, ow.data(), ow.size() * sizeof(double2), cudaMemcpyHostToDevice));
     T.G = std::min(F, 4 * 148);
     PD_CUDA(c, dalloc_d(&T.part, (size_t)T.G * H * Sg));
     if (c->dist_mode == 2) PD_CUDA(c, dalloc_d(&T.acc, (size_t)H * Sg));
   }
+  PD_CUDA(c, dalloc_c(&T.hc, (size_t)F * H));
+  PD_CUDA(c, cudaMemcpy(T.hc, hc.data(), hc.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  PD_CUDA(c, dalloc_c(&T.gx, (size_t)H * Sg));
   T.scr.assign(kScr, nullptr);
   for (auto& p : T.scr) PD_CUDA(c, dalloc_d(&p, (size_t)H * Sg));
   PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&T.flag), sizeof(int)));
@@ -231,6 +232,25 @@ pd_status dots(pd_ctx* c, std::vector<const double*> X, const double* y, long lo
   return pd_krylov_n(c, 0, X.data(), nullptr, (int)X.size(), 0.0, const_cast<double*>(y), n, out, false);
 }
 
+// u = P^{-1}(E_H g) (u += when acc), g replicated [H][Sg].  Single GPU: Step (a) of a head-only vector is the
+// weighted broadcast sum_t hc[n][t] g_t (of the x-transformed head in the fused 2D layout), so the forward time FFT
+// and the full-size right-hand side are skipped; sharded: the distributed apply of the embedded vector.
+pd_status apply_head(pd_ctx* c, const double* g, double* u, int acc) {
+  auto& T = c->tail;
+  const long long n = (long long)c->nt * c->S;
+  if (c->dist_mode != 0) {
+    PD_CUDA(c, cudaMemsetAsync(c->rvec, 0, sizeof(double) * n, c->st));
+    pd_status s = local_of(c, g, c->rvec);
+    return s != PD_OK ? s : pd_apply_impl(c, c->rvec, u, acc);
+  }
+  const long long Hn = (long long)T.H * c->S;
+  PD_LAUNCH(c, pd_launch_r2c(g, T.gx, Hn, c->st));
+  if (c->use_tfx) PD_LAUNCH(c, pd_launch_slab2d_rows(T.gx, c->g.nx, (long long)T.H * c->g.ny, 0, c->tw_s, c->st));
+  PD_LAUNCH(c, pd_launch_head_broadcast(c->Sh, c->F, c->S, T.H, T.hc, T.gx, c->st));
+  pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
+  return s != PD_OK ? s : pd_time_fft_inv(c, c->Sh, u, c->S, acc);
+}
+
 pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {
   PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * c->nt * c->S, c->st));
   if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
@@ -247,7 +267,8 @@ pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {
 
 void pd_tail_free(pd_ctx* c) {
   auto& T = c->tail;
-  for (void* p : {(void*)T.hc, (void*)T.ow, (void*)T.part, (void*)T.tau, (void*)T.work, (void*)T.flag, (void*)T.acc})
+  for (void* p : {(void*)T.hc, (void*)T.ow, (void*)T.part, (void*)T.tau, (void*)T.work, (void*)T.flag, (void*)T.acc,
+                  (void*)T.gx})
     if (p) cudaFree(p);
   for (double* p : T.scr) cudaFree(p);
   for (double* p : T.Vh) cudaFree(p);
@@ -280,14 +301,19 @@ pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double
   PD_TRY(pd_krylov_n(c, 0, &b, nullptr, 1, 0.0, const_cast<double*>(b), n, &bb));
   const double bnorm = std::sqrt(bb);
   if (bnorm == 0.0) return zero_report(c, u, rep);
-  double rr = 0;
-  PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // r^0 = b - A u^0
+  bool u_nz = true;
+  PD_TRY(any_nonzero(c, u, n, &u_nz));
+  double rr = bb;  // zero initial guess: r^0 = b
+  if (u_nz) PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // r^0 = b - A u^0
   double rel = std::sqrt(rr) / bnorm;
   int k = 0;
   if (rel > tol && maxit > 0) {
     double *tp = T.scr[0], *tc = T.scr[1], *yt = T.scr[2], *hd = T.scr[3], *dd = T.scr[4], *bh = T.scr[5];
     const long long tail_off = (long long)(c->nt - T.H) * c->S;
-    PD_TRY(gather_full(c, u + tail_off, tp));  // t^0
+    if (u_nz)
+      PD_TRY(gather_full(c, u + tail_off, tp));  // t^0
+    else
+      PD_CUDA(c, cudaMemsetAsync(tp, 0, sizeof(double) * Hn, c->st));
     bool nonhead = true;
     PD_TRY(any_nonzero(c, b + Hl, n - Hl, &nonhead));
     if (nonhead) {
@@ -313,14 +339,11 @@ pd_status pd_solve_stationary_tail(pd_ctx* c, const double* b, double* u, double
     }
     // u^k = P^{-1}(b + E_H G t^{k-1})
     PD_TRY(head_G(c, tp, hd));
-    PD_CUDA(c, cudaMemsetAsync(c->rvec, 0, sizeof(double) * n, c->st));
     if (nonhead) {
-      PD_TRY(local_of(c, hd, c->rvec));
-      PD_TRY(pd_apply_impl(c, c->rvec, u, 1));  // u = y + P^{-1}(E_H G t^{k-1})
+      PD_TRY(apply_head(c, hd, u, 1));  // u = y + P^{-1}(E_H G t^{k-1})
     } else {
       PD_TRY(comb(c, {bh, hd}, {1.0, 1.0}, hd, Hn));
-      PD_TRY(local_of(c, hd, c->rvec));
-      PD_TRY(pd_apply_impl(c, c->rvec, u, 0));
+      PD_TRY(apply_head(c, hd, u, 0));
     }
   }
   const bool conv = rel <= tol;
@@ -352,8 +375,14 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
   PD_TRY(pd_krylov_n(c, 0, &b, nullptr, 1, 0.0, const_cast<double*>(b), n, &bb));
   const double bnorm = std::sqrt(bb);
   if (bnorm == 0.0) return zero_report(c, u, rep);
-  double rr = 0;
-  PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // anchor r0 = b - A u0 (kept in rvec)
+  bool u_nz = true;
+  PD_TRY(any_nonzero(c, u, n, &u_nz));
+  double rr = bb;
+  const double* anchor = b;  // zero initial guess: r0 = b, read in place
+  if (u_nz) {
+    PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // anchor r0 = b - A u0 (kept in rvec)
+    anchor = c->rvec;
+  }
   double beta = std::sqrt(rr);
   int its = 0;
   bool conv = beta <= tol * bnorm, breakdown = false;
@@ -362,9 +391,13 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
   while (!conv && its < maxit) {
     bool nonhead = true;
-    PD_TRY(gather_full(c, c->rvec, r0h));  // replicated head of the anchor
-    PD_TRY(any_nonzero(c, c->rvec + Hl, n - Hl, &nonhead));
+    PD_TRY(gather_full(c, anchor, r0h));  // replicated head of the anchor
+    PD_TRY(any_nonzero(c, anchor + Hl, n - Hl, &nonhead));
     if (nonhead) {
+      if (anchor != c->rvec) {  // the final right-hand side scales the anchor in place
+        PD_CUDA(c, cudaMemcpyAsync(c->rvec, anchor, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->st));
+        anchor = c->rvec;
+      }
       PD_TRY(pd_apply_impl(c, c->rvec, c->zvec, 0));  // q0 = G tail(P^{-1} r0)
       PD_TRY(gather_full(c, c->zvec + tail_off, tq));
       PD_TRY(head_G(c, tq, q0));
@@ -446,12 +479,19 @@ pd_status pd_solve_gmres_tail(pd_ctx* c, const double* b, double* u, double tol,
     for (int i = 0; i < kk; ++i) ca += y[i] * A[i];
     std::vector<const double*> Xc(T.Vh.begin(), T.Vh.begin() + kk);
     PD_TRY(comb(c, Xc, std::vector<double>(y.begin(), y.begin() + kk), ch, Hn));
-    // u += P^{-1}(ca r0 + E_H ch): the anchor buffer becomes the right-hand side (this rank's part of ch)
-    PD_LAUNCH(c, pd_launch_axpby(c->rvec, c->rvec, ca, 0.0, n, c->st));
-    PD_TRY(local_of(c, ch, gt));
-    PD_TRY(comb(c, {c->rvec, gt}, {1.0, 1.0}, c->rvec, Hl));
-    PD_TRY(pd_apply_impl(c, c->rvec, u, 1));
+    if (!nonhead) {
+      // anchor supported on the head: u += P^{-1}(E_H (ca r0h + ch)) without a full-size right-hand side
+      PD_TRY(comb(c, {r0h, ch}, {ca, 1.0}, ch, Hn));
+      PD_TRY(apply_head(c, ch, u, 1));
+    } else {
+      // u += P^{-1}(ca r0 + E_H ch): the anchor buffer becomes the right-hand side (this rank's part of ch)
+      PD_LAUNCH(c, pd_launch_axpby(c->rvec, c->rvec, ca, 0.0, n, c->st));
+      PD_TRY(local_of(c, ch, gt));
+      PD_TRY(comb(c, {c->rvec, gt}, {1.0, 1.0}, c->rvec, Hl));
+      PD_TRY(pd_apply_impl(c, c->rvec, u, 1));
+    }
     PD_TRY(pd_stencil_impl(c, b, u, c->rvec, &rr));  // true residual; the next cycle's anchor
+    anchor = c->rvec;
     beta = std::sqrt(rr);
     conv = beta <= tol * bnorm;
     if (breakdown) break;
