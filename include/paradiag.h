@@ -178,6 +178,14 @@ PD_API pd_status pd_apply_precond_host(pd_ctx* ctx, const double* r_host, double
 PD_API pd_status pd_solve_host(pd_ctx* ctx, int solver /*0 stationary, 1 gmres*/, const double* b_host,
                         double* u_host, double tol, int m, int maxit, pd_report* rep);
 
+/* End-to-end solve of the initial-value problem from HOST initial data: copy u0 [S] (v0 [S] for leapfrog, may
+ * be NULL = 0; f [(Nt+1)][S] sampled at t_n = n dt, may be NULL = 0) to the device, build b there
+ * (pd_build_rhs), solve from u = 0, copy the space-time solution [Nt][S] to u_host, synchronise.
+ * solver: 0 stationary, 1 GMRES, 2 stationary tail form, 3 GMRES tail form, 4 simplified Newton (needs
+ * pd_set_reaction).  Host->device traffic is the initial data only. */
+PD_API pd_status pd_solve_ivp_host(pd_ctx* ctx, int solver, const double* u0_host, const double* v0_host,
+                                   const double* f_host, double* u_host, double tol, int m, int maxit, pd_report* rep);
+
 /* Number of kernels this context has launched so far (for the bench's gpu_launches claim). */
 PD_API long long pd_kernel_launches(const pd_ctx* ctx);
 

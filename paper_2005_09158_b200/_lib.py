@@ -81,6 +81,7 @@ def load_library(path: str | None = None):
         "pd_solve_gmres_tail": (ip, [vp, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_set_reaction": (ip, [vp, C.c_double, C.c_double]),
         "pd_solve_newton": (ip, [vp, vp, vp, C.c_double, ip, C.POINTER(pd_report)]),
+        "pd_solve_ivp_host": (ip, [vp, ip, vp, vp, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_apply_precond_host": (ip, [vp, vp, vp]),
         "pd_solve_host": (ip, [vp, ip, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_kernel_launches": (C.c_longlong, [vp]),
@@ -305,6 +306,16 @@ class ParaDiag:
         _check(self._lib, self._ctx, self._lib.pd_apply_precond_host(
             self._ctx, C.c_void_p(r_host.data_ptr()), C.c_void_p(z_host.data_ptr())))
         return z_host
+
+    def solve_ivp_host(self, solver: int, u0_host, u_host, v0_host=None, f_host=None, tol=1e-10, m=20, maxit=100):
+        """End to end from HOST initial data (pinned CPU float64 tensors); u_host [Nt, S] receives the solution.
+        solver: 0 stationary, 1 GMRES, 2 / 3 their tail forms, 4 simplified Newton."""
+        rep, hist = self._report(maxit + 2)
+        p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+        st = self._lib.pd_solve_ivp_host(self._ctx, solver, p(u0_host), p(v0_host), p(f_host), p(u_host), tol, m,
+                                         maxit, C.byref(rep))
+        _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
+        return u_host, self._mk(st, rep, hist)
 
     def solve_host(self, solver: int, b_host, u_host, tol, m=20, maxit=100):
         rep, hist = self._report(maxit + 2)

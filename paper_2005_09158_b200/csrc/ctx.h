@@ -99,6 +99,8 @@ struct pd_ctx {
   double* zvec = nullptr;
   double* gm_head = nullptr;     // head-sized work vector of the corner-identity GMRES path
   int* gm_flag = nullptr;        // zero-initial-guess check
+  double* ivp_init = nullptr;    // pd_solve_ivp_host: u0, v0 on the device
+  double* ivp_f = nullptr;       // pd_solve_ivp_host: source samples
   int* gm_hflag = nullptr;
   // host-buffer staging
   double* stage_a = nullptr;

@@ -173,6 +173,8 @@ static void free_ctx(pd_ctx* c) {
   if (c->nl_dbar) cudaFree(c->nl_dbar);
   if (c->gm_head) cudaFree(c->gm_head);
   if (c->gm_flag) cudaFree(c->gm_flag);
+  if (c->ivp_init) cudaFree(c->ivp_init);
+  if (c->ivp_f) cudaFree(c->ivp_f);
   if (c->gm_hflag) cudaFreeHost(c->gm_hflag);
   if (c->nl_cp) cudaFree(c->nl_cp);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
@@ -1051,6 +1053,39 @@ pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, dou
   solver &= ~PD_SOLVE_ZERO_GUESS;
   s = solver == 0 ? pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep)
                   : pd_solve_gmres(c, c->stage_a, c->stage_b, tol, m, maxit, rep);
+  if (s < 0) return s;
+  PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  return s;
+}
+
+pd_status pd_solve_ivp_host(pd_ctx* c, int solver, const double* u0h, const double* v0h, const double* fh, double* uh,
+                            double tol, int m, int maxit, pd_report* rep) {
+  if (!c || !u0h || !uh) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  if (solver < 0 || solver > 4) return fail(c, PD_EINVAL, "solver %d not in 0..4", solver);
+  pd_status s = ensure_stage(c);
+  if (s != PD_OK) return s;
+  const size_t Sb = sizeof(double) * c->S, bytes = Sb * c->nt;
+  if (!c->ivp_init && dalloc(&c->ivp_init, (size_t)2 * c->S + 2) != cudaSuccess) return fail(c, PD_ENOMEM, "ivp buffers");
+  double *du0 = c->ivp_init, *dv0 = c->ivp_init + c->S;
+  PD_CUDA(c, cudaMemcpyAsync(du0, u0h, Sb, cudaMemcpyHostToDevice, c->st));
+  if (v0h) PD_CUDA(c, cudaMemcpyAsync(dv0, v0h, Sb, cudaMemcpyHostToDevice, c->st));
+  double* df = nullptr;
+  if (fh) {
+    if (!c->ivp_f && dalloc(&c->ivp_f, (size_t)(c->nt + 1) * c->S) != cudaSuccess) return fail(c, PD_ENOMEM, "ivp f");
+    df = c->ivp_f;
+    PD_CUDA(c, cudaMemcpyAsync(df, fh, Sb * (c->nt + 1), cudaMemcpyHostToDevice, c->st));
+  }
+  s = pd_build_rhs(c, du0, v0h ? dv0 : nullptr, df, c->stage_a);
+  if (s != PD_OK) return s;
+  PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
+  switch (solver) {
+    case 0: s = pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
+    case 1: s = pd_solve_gmres(c, c->stage_a, c->stage_b, tol, m, maxit, rep); break;
+    case 2: s = pd_solve_stationary_tail(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
+    case 3: s = pd_solve_gmres_tail(c, c->stage_a, c->stage_b, tol, m, maxit, rep); break;
+    default: s = pd_solve_newton(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
+  }
   if (s < 0) return s;
   PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
   PD_CUDA(c, cudaStreamSynchronize(c->st));

@@ -281,3 +281,23 @@ def test_gmres_corner_identity_equals_matvec_path(name, monkeypatch):
     assert rel(to_host(u1), to_host(u2)) < 1e-10 and rel(to_host(u3), to_host(u2)) < 1e-10
     for a, c in zip(r1.history, r2.history):
         assert abs(a - c) <= 1e-6 * c + 1e-14
+
+
+
+@pytest.mark.parametrize("name,solver", [("cfg1", 1), ("cfg1", 3), ("cfg2", 0), ("cfg2", 2), ("cfg0", 0)])
+def test_solve_ivp_host_matches_oracle(name, solver):
+    """pd_solve_ivp_host: host initial data (u0, v0, source samples) in, b built on the device, the space-time
+    solution out - same counts and solution as the oracle for every solver code."""
+    import torch
+    cfg = W.BY_NAME[name]
+    u0, v0, f = W.initial_u0(cfg), W.initial_v0(cfg), W.source_samples(cfg)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    ctx = make_ctx(cfg)
+    uh = torch.empty(ctx.shape, dtype=torch.float64).pin_memory()
+    _, rep = ctx.solve_ivp_host(solver, pin(u0), uh, pin(v0) if cfg.op == W.WAVE1D else None,
+                                pin(f) if f is not None else None, cfg.tol, cfg.m, cfg.maxit)
+    b = problems.rhs(cfg, u0, v0, f)
+    fn = solvers.solve_stationary if solver in (0, 2) else solvers.solve_gmres
+    u_ref, rep_ref = fn(cfg, b)
+    assert rep.converged and rep.iterations == rep_ref.iterations
+    assert rel(uh.numpy(), u_ref) < SOLVE_TOL
