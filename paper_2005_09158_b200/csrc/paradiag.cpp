@@ -848,7 +848,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
   std::vector<const double*> Xv(c->V.begin(), c->V.end());
   double rr = 0;
   bool u_zero = false;
-  if (c->dist_mode == 0) {
+  if (c->dist_mode == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {  // b read in place by the Krylov kernels
     if (!c->gm_flag) {
       PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->gm_flag), sizeof(int)));
       PD_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->gm_hflag), sizeof(int)));
