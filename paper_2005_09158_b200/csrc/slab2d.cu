@@ -150,15 +150,17 @@ cudaError_t launch_n(double2* Sh, int nfreq, const double2* lam1, const double2*
                      cudaStream_t st, int* launches) {
   using T = SlabCfg<N>;
   const int smem = smem_bytes<N>();
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(slab_rows_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_cols_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cols<N>());
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   int nl = 0;
   for (int s0 = 0; s0 < nfreq; s0 += chunk) {
@@ -277,13 +279,15 @@ cudaError_t dst_n(double2* Sh, int nfreq, const double2* lam1, const double2* la
   using T = SlabCfg<M>;
   constexpr int N = M / 2 - 1;
   const int smr = smem_bytes<M>(), smc = smem_cols<M>();
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(dst_rows_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dst_rows_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dst_cols_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smc);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   int nl = 0;
   for (int s0 = 0; s0 < nfreq; s0 += chunk) {
@@ -429,15 +433,17 @@ cudaError_t ytri_n(double2* Sh, int nfreq, int f0g, const pd_ytri_coef* coef, do
                    int chunk, int rows, cudaStream_t st, int* launches) {
   using T = SlabCfg<N>;
   const int smem = kYC * (N + 33) * (int)sizeof(double2), smr = smem_bytes<N>();
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(slab_ytri_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_rows_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   int nl = 0;
   for (int s0 = 0; s0 < nfreq; s0 += chunk) {
@@ -457,15 +463,17 @@ template <int N>
 cudaError_t filter_n(double2* slab, const double2* tab, const double2* tw, cudaStream_t st) {
   using T = SlabCfg<N>;
   const int smem = smem_bytes<N>();
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(slab_rows_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_rows_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_cols_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cols<N>());
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   slab_rows_kernel<N, false><<<N / T::C, T::NTH, smem, st>>>(slab, tw);
   slab_cols_kernel<N, true><<<dim3(N / ColCfg<N>::C, 1), ColCfg<N>::NTH, smem_cols<N>(), st>>>(slab, 0, nullptr, nullptr, nullptr,

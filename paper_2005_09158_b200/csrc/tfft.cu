@@ -175,11 +175,13 @@ cudaError_t launch_fwd_n(const double* r, double2* Sh, long long S, const double
                          cudaStream_t st) {
   using T = TileCfg<N>;
   const int smem = smem_elems(N * T::C) * (int)sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(tfft_fwd_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   const long long tiles = (S + 2 * T::C - 1) / (2 * T::C);
   tfft_fwd_kernel<N><<<(unsigned)tiles, T::NTH, smem, st>>>(r, Sh, S, gam, tw);
@@ -191,13 +193,15 @@ cudaError_t launch_inv_n(const double2* Sh, double* z, long long S, const double
                          int accumulate, cudaStream_t st) {
   using T = TileCfg<N>;
   const int smem = smem_elems((N / 2 + 1) * 2 * T::C) * (int)sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(tfft_inv_kernel<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(tfft_inv_kernel<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   const long long tiles = (S + 2 * T::C - 1) / (2 * T::C);
   if (accumulate)

@@ -180,12 +180,14 @@ void fwd_grid(const double* r, double2* Sh, long long S, const double* gam, cons
               double2* scratch, long long p, long long pc, bool vec, cudaStream_t st) {
   constexpr int N1 = NT / kN2;
   const int sm1 = smem_of<kN2>(kP), sm2 = smem_of<N1>(2 * kP);
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaFuncSetAttribute(tf4_fwd_s1<NT, kN2, kP, true, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(tf4_fwd_s1<NT, kN2, kP, false, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(tf4_fwd_s2<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    attr = true;
+    attr = dev_;
   }
   const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
   const dim3 g1(nt1, N1), g2(nt1, kN2 / 2 + 1);
@@ -204,14 +206,16 @@ void inv_grid(const double2* Sh, double* z, long long S, const double* igam, con
                       ? smem_of<N1>(2 * kP)
                       : smem_elems(2 * N1 * 2 * kP) * (int)sizeof(double2);
   const int sm2 = smem_of<kN2>(kP);
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaFuncSetAttribute(tf4_inv_s1<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, true, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, true, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, false, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, false, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    attr = true;
+    attr = dev_;
   }
   const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
   const dim3 g1(nt1, kN2 / 2 + 1), g2(nt1, N1);

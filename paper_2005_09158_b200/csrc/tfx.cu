@@ -215,8 +215,10 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1(const
 template <int NT, int NX>
 void set_attrs() {
   using F = Fx<NT, NX>;
-  static bool done = false;
-  if (done) return;
+  static int done = -1;  // device on which the attributes were set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done == dev) return;
   constexpr int N2 = F::N2, KP = F::KP;
   const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, true, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
@@ -227,7 +229,7 @@ void set_attrs() {
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 1, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, false, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, false, 1, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
-  done = true;
+  done = dev;
 }
 
 template <int NT, int NX>

@@ -227,11 +227,13 @@ __global__ void __launch_bounds__(NT) tail1d_kernel(const double* __restrict__ g
 template <int NT>
 cudaError_t launch_nt(double2* Sh, int nx, int nfreq, const pd_tri_coef* coef, cudaStream_t st) {
   const int smem = (NT * kL + NT) * (int)sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
     cudaError_t e = cudaFuncSetAttribute(tridiag_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = dev_;
   }
   tridiag_kernel<NT><<<nfreq, NT, smem, st>>>(Sh, nx, coef);
   return cudaGetLastError();
