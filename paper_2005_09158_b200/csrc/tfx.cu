@@ -103,21 +103,25 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2(const
       });
   __syncthreads();
   // (3) untangle the two real columns of each pair and combine the even/odd halves into X_n[kx]
+  // row-level index work hoisted out of the element loop (uniform across the CTA)
   const int nsets = n2p == n2 ? 1 : 2;
-  const int total = nsets * N1 * NX;
-  for (int o = threadIdx.x; o < total; o += NTH) {
-    const int kx = o & (NX - 1);
-    const int rowi = o / NX, set = rowi / N1, n1 = rowi % N1;
+  for (int rowi = 0; rowi < nsets * N1; ++rowi) {
+    const int set = rowi / N1, n1 = rowi % N1;
     const int n = (set ? n2p : n2) + N2 * n1;
     if (n > NT / 2) continue;
     const int m = (NT - n) & (NT - 1);
     const int setp = (m % N2) == n2 ? 0 : 1, n1p = m / N2;
-    const int k = kx & (NP - 1);
-    const double2 a = sm[pad((2 * n1 + set) * NP + k)];
-    const double2 b = sm[pad((2 * n1p + setp) * NP + ((NP - k) & (NP - 1)))];
-    const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));     // (a + conj b) / 2
-    const double2 O = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));    // (a - conj b) / 2i
-    __stcs(Sh + (long long)n * S + 2 * p0 + kx, cfma(PD_TFX_TWX_SMEM ? s_twx[kx] : __ldg(twx + kx), O, E));
+    const int ra = (2 * n1 + set) * NP, rb = (2 * n1p + setp) * NP;
+    double2* out = Sh + (long long)n * S + 2 * p0;
+#pragma unroll
+    for (int kx = threadIdx.x; kx < NX; kx += NTH) {
+      const int k = kx & (NP - 1);
+      const double2 a = sm[pad(ra + k)];
+      const double2 b = sm[pad(rb + ((NP - k) & (NP - 1)))];
+      const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));     // (a + conj b) / 2
+      const double2 O = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));    // (a - conj b) / 2i
+      __stcs(out + kx, cfma(PD_TFX_TWX_SMEM ? s_twx[kx] : __ldg(twx + kx), O, E));
+    }
   }
 }
 
