@@ -301,3 +301,26 @@ def test_solve_ivp_host_matches_oracle(name, solver):
     u_ref, rep_ref = fn(cfg, b)
     assert rep.converged and rep.iterations == rep_ref.iterations
     assert rel(uh.numpy(), u_ref) < SOLVE_TOL
+
+
+def test_error_paths_of_the_extensions():
+    """PD_EINVAL (never a silent fallback) for calls outside what each entry point supports."""
+    import torch
+    from paper_2005_09158_b200 import ParaDiagError
+    c2 = make_ctx(W.CONFIGS[3].scaled(nx=16, ny=16, nt=8))
+    with pytest.raises(ParaDiagError):
+        c2.set_reaction(1.0, -1.0)                      # reaction terms: 1D theta-method only
+    cw = make_ctx(W.CONFIGS[2].scaled(nx=31, nt=8))
+    with pytest.raises(ParaDiagError):
+        cw.set_reaction(1.0, -1.0)                      # not for leapfrog
+    c1 = make_ctx(W.CONFIGS[0])
+    u0 = torch.from_numpy(W.initial_u0(W.CONFIGS[0])).pin_memory()
+    uh = torch.empty(c1.shape, dtype=torch.float64).pin_memory()
+    with pytest.raises(ParaDiagError):
+        c1.solve_ivp_host(7, u0, uh)                    # unknown solver code
+    with pytest.raises(ParaDiagError):
+        c1.solve_gmres(to_dev(np.ones(c1.shape)), m=31)  # m > 30
+    with pytest.raises(ParaDiagError):
+        make_ctx(W.t4a_config(32).scaled(nx=32, ny=32))  # 2D Dirichlet needs N + 1 a power of two
+    with pytest.raises(ParaDiagError):
+        make_ctx(W.t4a_config(32), rank=-1, size=2).solve_newton(to_dev(np.ones((32, 961))))  # Newton: 1D only
