@@ -2,7 +2,7 @@
 
 Writes profiles/ncu_traffic.json {cfg: {phase: bytes per call}} used by bench.py's roofline.traffic.  Per-launch
 dram__bytes_read.sum + dram__bytes_write.sum of each kernel, times the launches one phase call makes at cfg4
-(time FFTs: 4 chunks of 32768 pairs; column pass: 4 chunks of 256 slabs + 1 slab)."""
+(time FFTs: 4 chunks of 32768 pairs; y-pass: 4 chunks of 256 slabs + 1 slab)."""
 import csv, json, os, subprocess, sys, collections
 per = collections.defaultdict(list)
 for rep in sys.argv[1:]:
@@ -20,7 +20,7 @@ def get(prefix, pick=max):
     return pick(per[ks[0]]) if ks else None
 fwd = 4 * (get("pdfft_tf4::tf4_fwd_s1<2048") + get("tfx_fwd_s2<2048"))
 inv = 4 * (get("tfx_inv_s1<2048") + get("pdfft_tf4::tf4_inv_s2<2048, 256, 16, 1, 0"))
-cols = 4 * get("slab_cols_kernel<512, 0>") + get("slab_cols_kernel<512, 0>", min)
+cols = get("slab_ytri_kernel<512>") / 256 * 1025  # y-pass: per-slab bytes of a 256-slab chunk x F = 1025 slabs
 out = {"cfg4": {"tfft_fwd": fwd, "spatial_solve": cols, "tfft_inv": inv},
        "source": "ncu --set full --clock-control none, tools/prof_apply.py --config cfg4 (r01); per call = per-launch "
                  "dram read+write x launches per call",
