@@ -83,6 +83,9 @@ int pd_slab2d_ytri_supported(int n);
 // 2D homogeneous Dirichlet (PD_WAVE2D_DIRICHLET): N = 2^k - 1 interior nodes; tensor DST-I via FFTs of length
 // M = 2(N+1) of the odd extension; mu[k] = (4 nu/h^2) sin^2(pi k/M), k < M; tw: M-point twiddles
 int pd_slab2d_dst_supported(int n);
+// out[n] = min over (kx, ky) of |lam1_n + lam2_n kappa| / (|lam1_n| + |lam2_n| |kappa|)  (setup singularity check)
+cudaError_t pd_launch_min_den(const double2* lam1, const double2* lam2, const double* sx, const double* sn,
+                              pd_slab_params prm, int n, int nfreq, double* out, cudaStream_t st);
 cudaError_t pd_launch_slab2d_dst(double2* Sh, int n, int nfreq, const double2* lam1, const double2* lam2,
                                  const double* mu, const double2* tw, int chunk, cudaStream_t st, int* launches);
 int pd_slab2d_chunk(int n, int nfreq);

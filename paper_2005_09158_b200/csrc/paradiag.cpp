@@ -393,25 +393,8 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
       hsx[k] = (double)(sk * sk);
       hsn[k] = (double)sinl(2.0L * pi * k / N);
     }
-    // singularity: min |lambda1 + lambda2 kappa| over the half spectrum and all (kx, ky)
-    long double worst = 1e300L;
-    int wn = -1;
-    for (int n = 0; n < c->F; ++n) {
-      for (int ky = 0; ky < N; ++ky)
-        for (int kx = 0; kx < N; ++kx) {
-          const cld kap((long double)c->slab.kd * (hsx[kx] + hsx[ky]),
-                        (long double)c->slab.cx * hsn[kx] + (long double)c->slab.cy * hsn[ky]);
-          const long double m = std::abs(l1[n] + l2[n] * kap) / (std::abs(l1[n]) + std::abs(l2[n]) * std::abs(kap) + 1e-300L);
-          if (m < worst) {
-            worst = m;
-            wn = n;
-          }
-        }
-    }
-    if (worst < 1e-13L) {
-      free_ctx(c);
-      return fail(nullptr, PD_ESINGULAR, "shifted system singular at frequency n=%d (relative |den| %.3Le)", wn, worst);
-    }
+    // singularity: min |lambda1 + lambda2 kappa| / (|lambda1| + |lambda2| |kappa|) over the half spectrum and all
+    // (kx, ky) - an F N^2 reduction, done on the device (min_den_kernel) once the tables are there (below)
     std::vector<double2> htws = twiddles(N);
     SETUP_CUDA(dalloc(&c->sx, N));
     SETUP_CUDA(dalloc(&c->sn, N));
@@ -419,6 +402,22 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     SETUP_CUDA(cudaMemcpy(c->sx, hsx.data(), N * sizeof(double), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->sn, hsn.data(), N * sizeof(double), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->tw_s, htws.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
+    {
+      double* dmin = nullptr;
+      SETUP_CUDA(dalloc(&dmin, (size_t)c->F));
+      SETUP_CUDA(pd_launch_min_den(c->lam1, c->lam2, c->sx, c->sn, c->slab, N, c->F, dmin, c->st));
+      std::vector<double> hmin(c->F);
+      SETUP_CUDA(cudaMemcpyAsync(hmin.data(), dmin, c->F * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      SETUP_CUDA(cudaStreamSynchronize(c->st));
+      cudaFree(dmin);
+      int wn = 0;
+      for (int n = 1; n < c->F; ++n)
+        if (hmin[n] < hmin[wn]) wn = n;
+      if (hmin[wn] < 1e-13) {
+        free_ctx(c);
+        return fail(nullptr, PD_ESINGULAR, "shifted system singular at frequency n=%d (relative |den| %.3e)", wn, hmin[wn]);
+      }
+    }
     c->slab_chunk = pd_slab2d_chunk(N, c->F);
     // y-pass by cyclic Toeplitz solves where every column is in the stable regime (PD_NO_YTRI: FFT column pass)
     if (pd_slab2d_ytri_supported(N) && getenv("PD_NO_YTRI") == nullptr) {

@@ -526,6 +526,37 @@ cudaError_t pd_launch_slab2d_filter(double2* slab, int n, const double2* tab, co
   }
 }
 
+// setup check (host calls once): out[n] = min over (kx, ky) of |l1 + l2 kappa| / (|l1| + |l2| |kappa|)
+__global__ void min_den_kernel(const double2* __restrict__ lam1, const double2* __restrict__ lam2,
+                               const double* __restrict__ sx, const double* __restrict__ sn, pd_slab_params prm, int N,
+                               double* __restrict__ out) {
+  __shared__ double red[256];
+  const int n = blockIdx.x;
+  const double2 l1 = lam1[n], l2 = lam2[n];
+  const double a1 = hypot(l1.x, l1.y), a2 = hypot(l2.x, l2.y);
+  double m = 1e300;
+  const long long NN = (long long)N * N;
+  for (long long i = threadIdx.x; i < NN; i += blockDim.x) {
+    const int kx = (int)(i % N), ky = (int)(i / N);
+    const double2 kap = make_double2(prm.kd * (sx[kx] + sx[ky]), prm.cx * sn[kx] + prm.cy * sn[ky]);
+    const double2 d = cfma(l2, kap, l1);
+    m = fmin(m, hypot(d.x, d.y) / (a1 + a2 * hypot(kap.x, kap.y) + 1e-300));
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s2 = 128; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s2]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = red[0];
+}
+
+cudaError_t pd_launch_min_den(const double2* lam1, const double2* lam2, const double* sx, const double* sn,
+                              pd_slab_params prm, int n, int nfreq, double* out, cudaStream_t st) {
+  min_den_kernel<<<nfreq, 256, 0, st>>>(lam1, lam2, sx, sn, prm, n, out);
+  return cudaGetLastError();
+}
+
 int pd_slab2d_dst_supported(int n) {
   return n == 15 || n == 31 || n == 63 || n == 127 || n == 255 || n == 511;
 }

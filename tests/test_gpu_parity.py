@@ -324,3 +324,15 @@ def test_error_paths_of_the_extensions():
         make_ctx(W.t4a_config(32).scaled(nx=32, ny=32))  # 2D Dirichlet needs N + 1 a power of two
     with pytest.raises(ParaDiagError):
         make_ctx(W.t4a_config(32), rank=-1, size=2).solve_newton(to_dev(np.ones((32, 961))))  # Newton: 1D only
+
+
+@pytest.mark.parametrize("cfg", [W.CONFIGS[0].scaled(nx=15, nt=8, nu=0.0, ax=0.0, alpha=1.0),
+                                 W.CONFIGS[3].scaled(nx=16, ny=16, nt=8, nu=0.0, ax=0.0, ay=0.0, alpha=1.0),
+                                 W.t4a_config(32, 1.0, nu=0.0, scheme=W.BE)])
+def test_singular_shift_reported(cfg):
+    """alpha = 1 and K = 0: lambda_1 at n = 0 vanishes, so the n = 0 shifted system is exactly singular (S:l.77):
+    pd_setup reports PD_ESINGULAR and names the frequency, for every Step (b) family."""
+    from paper_2005_09158_b200 import ParaDiagError
+    with pytest.raises(ParaDiagError) as ei:
+        make_ctx(cfg)
+    assert ei.value.status == -2 and "n=0" in str(ei.value)
