@@ -43,6 +43,15 @@ constexpr int kRX = PD_TFX_RM;
 #ifndef PD_TFX_TWX_SMEM
 #define PD_TFX_TWX_SMEM 1  // NX-point twiddles staged in smem (0: read through L1)
 #endif
+#ifndef PD_TFX_XFIRST
+#define PD_TFX_XFIRST 1    // x-FFT before the N1-point time DFT (tfx_fwd_s2x / tfx_inv_s1x); 0: the t1-first kernels
+#endif
+#ifndef PD_TFX_XFIRST_FWD
+#define PD_TFX_XFIRST_FWD PD_TFX_XFIRST
+#endif
+#ifndef PD_TFX_XFIRST_INV
+#define PD_TFX_XFIRST_INV PD_TFX_XFIRST
+#endif
 constexpr int kRS = PD_TFX_S1_RM;
 
 template <int NT, int NX>
@@ -216,6 +225,195 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1(const
       });
 }
 
+// ---------------------------------------------------------------------------------------------
+// x-first variants (PD_TFX_XFIRST): the N1-point DFT over t1 commutes with the NP-point FFT over p
+// (the four-step twiddle w_Nt^{t1 n2} is already applied in stage 1 / applied after, per row), so the
+// x-FFT runs first and one thread per index k then does the N1-point DFTs of column k of residue set 0
+// and of the mirror column NP - k of the partner set, which is exactly what the even/odd untangle pairs
+// (row n with row Nt - n at index -k).  The untangle and the N1-point DFTs stay in registers: 2 smem
+// writes + 2 reads per element instead of 3 + 3.
+// ---------------------------------------------------------------------------------------------
+// Mirror rows: n = r + N2 n1 of residue r has Nt - n = (N2 - r) + N2 (N1 - 1 - n1) for r > 0 (the partner
+// set) and N2 ((N1 - n1) mod N1) for r = 0 (the same set).
+// X_n[i] = E + w^i O, X_n[i + NP] = E - w^i O;  E = (x + conj y) / 2, O = (x - conj y) / 2i, y = A_{Nt-n}[-i]
+template <int NP>
+PD_D void untangle_store(double2* out, int i, double2 x, double2 y, double2 w) {
+  const double2 E = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+  const double2 O = make_double2(0.5 * (x.y + y.y), -0.5 * (x.x - y.x));
+  const double2 wO = cmul(w, O);
+  __stcs(out + i, cadd(E, wO));
+  __stcs(out + i + NP, csub(E, wO));
+}
+
+template <int NT, int NX>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(const double2* __restrict__ Y, long long S,
+                                                              long long p_begin, long long Pc,
+                                                              double2* __restrict__ Sh,
+                                                              const double2* __restrict__ twx) {
+  using F = Fx<NT, NX>;
+  constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_twx[NP], s_twp[NP];
+  const int n2 = blockIdx.y, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
+  const long long pl0 = (long long)blockIdx.x * NP;
+  const long long p0 = p_begin + pl0;
+  for (int i = threadIdx.x; i < NX; i += NTH) {
+    const double2 w = __ldg(twx + i);
+    if (i < NP) s_twx[i] = w;
+    if (!(i & 1)) s_twp[i >> 1] = w;
+  }
+  // (1) NP-point FFTs over p of the 2 N1 rows c = (set, t1) straight from Y[t1][n2][pair]
+  fft_io<NP, 2 * N1, false, true, NTH, false, true, kRX>(
+      sm, s_twp,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(NP, kRX);
+        const int set = c / N1, t1 = c % N1;
+        const double2* q = Y + ((long long)t1 * N2 + (set ? n2p : n2)) * Pc + pl0 + j;
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = __ldcg(q + m * s);
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(NP, kRX);
+#pragma unroll
+        for (int m = 0; m < RL; ++m) sm[pad(c * NP + j + m * s)] = w[m];
+      });
+  __syncthreads();
+  // (2) N1-point DFTs over t1 of column k (set 0) and column NP - k (partner set), untangle, store
+  const int sb = nsets == 2 ? 1 : 0;
+  for (int k = threadIdx.x; k < NP; k += NTH) {
+    const int kb = (NP - k) & (NP - 1);
+    double2 a[N1], b[N1];
+#pragma unroll
+    for (int t = 0; t < N1; ++t) {
+      a[t] = sm[pad(t * NP + k)];
+      b[t] = sm[pad((sb * N1 + t) * NP + kb)];
+    }
+    DFT<N1, false>::run(a);
+    DFT<N1, false>::run(b);
+    const double2 wk = s_twx[k], wb = s_twx[kb];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int n = n2 + N2 * n1;
+      if (n <= NT / 2) {
+        const double2 y = n2 == 0 ? b[(N1 - n1) & (N1 - 1)] : b[N1 - 1 - n1];
+        untangle_store<NP>(Sh + (long long)n * S + 2 * p0, k, a[n1], y, wk);
+      }
+    }
+    if (nsets == 2) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int n = n2p + N2 * n1;
+        if (n <= NT / 2) untangle_store<NP>(Sh + (long long)n * S + 2 * p0, kb, b[n1], a[N1 - 1 - n1], wb);
+      }
+    }
+  }
+}
+
+// A_n[i] = E + iO from X_n[i], X_n[i + NP]:  E = x0 + x1, O = (x0 - x1) w^-i;  the mirror row
+// A_{Nt-n}[-i] = conj(E - iO)
+PD_D double2 a_direct(double2 x0, double2 x1, double2 wi) {
+  const double2 E = cadd(x0, x1), O = cmulc(csub(x0, x1), wi);
+  return make_double2(E.x - O.y, E.y + O.x);
+}
+PD_D double2 a_mirror(double2 x0, double2 x1, double2 wi) {
+  const double2 E = cadd(x0, x1), O = cmulc(csub(x0, x1), wi);
+  return make_double2(E.x + O.y, O.x - E.y);
+}
+
+template <int NT, int NX>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(const double2* __restrict__ Sh, long long S,
+                                                              long long p_begin, long long Pc,
+                                                              double2* __restrict__ W,
+                                                              const double2* __restrict__ twx,
+                                                              const double2* __restrict__ twt) {
+  using F = Fx<NT, NX>;
+  constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
+  constexpr int NV = N1 / 2 + 1;  // rows n = r + N2 n1 <= Nt/2 have n1 <= N1/2
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_twx[NP], s_twp[NP], s_twa[N1], s_twb[N1];
+  const int n2 = blockIdx.y, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
+  const int rb = nsets == 2 ? n2p : n2;  // residue of the partner set (self-partnered: the same set)
+  const long long pl0 = (long long)blockIdx.x * NP;
+  const long long p0 = p_begin + pl0;
+  for (int i = threadIdx.x; i < NX; i += NTH) {
+    const double2 w = __ldg(twx + i);
+    if (i < NP) s_twx[i] = w;
+    if (!(i & 1)) s_twp[i >> 1] = w;
+  }
+  if (threadIdx.x < N1) {
+    s_twa[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2));
+    s_twb[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2p));
+  }
+  __syncthreads();
+  // (0) per k: the stored rows n <= Nt/2 of set 0 at k and of the partner set at NP - k give every row of
+  // set 0 at k and of the partner set at NP - k (direct or mirror); N1-point inverse DFTs over n1 -> smem
+  for (int k = threadIdx.x; k < NP; k += NTH) {
+    const int kb = (NP - k) & (NP - 1);
+    double2 x0[NV], x1[NV], y0[NV], y1[NV];
+#pragma unroll
+    for (int n1 = 0; n1 < NV; ++n1) {
+      const int na = n2 + N2 * n1, nb = rb + N2 * n1;
+      if (na <= NT / 2) {
+        const double2* q = Sh + (long long)na * S + 2 * p0 + k;
+        x0[n1] = __ldcs(q);
+        x1[n1] = __ldcs(q + NP);
+      }
+      if (nb <= NT / 2) {
+        const double2* q = Sh + (long long)nb * S + 2 * p0 + kb;
+        y0[n1] = __ldcs(q);
+        y1[n1] = __ldcs(q + NP);
+      }
+    }
+    const double2 wk = s_twx[k], wb = s_twx[kb];
+    double2 a[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      if (n1 < NV && n2 + N2 * n1 <= NT / 2) {
+        a[n1] = a_direct(x0[n1 < NV ? n1 : 0], x1[n1 < NV ? n1 : 0], wk);
+      } else {  // partner row (N1 - n1) mod N1 for r = 0, N1 - 1 - n1 for r > 0 (compile-time indices)
+        const int ma = ((N1 - n1) & (N1 - 1)) < NV ? ((N1 - n1) & (N1 - 1)) : 0;
+        const int mb = (N1 - 1 - n1) < NV ? (N1 - 1 - n1) : 0;
+        a[n1] = n2 == 0 ? a_mirror(y0[ma], y1[ma], wb) : a_mirror(y0[mb], y1[mb], wb);
+      }
+    }
+    DFT<N1, true>::run(a);
+#pragma unroll
+    for (int t = 0; t < N1; ++t) sm[pad(t * NP + k)] = a[t];
+    if (nsets == 2) {
+      double2 b[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int mb = N1 - 1 - n1;
+        if (n1 < NV && rb + N2 * n1 <= NT / 2)
+          b[n1] = a_direct(y0[n1 < NV ? n1 : 0], y1[n1 < NV ? n1 : 0], wb);
+        else
+          b[n1] = a_mirror(x0[mb < NV ? mb : 0], x1[mb < NV ? mb : 0], wk);
+      }
+      DFT<N1, true>::run(b);
+#pragma unroll
+      for (int t = 0; t < N1; ++t) sm[pad((N1 + t) * NP + kb)] = b[t];
+    }
+  }
+  __syncthreads();
+  // (1) NP-point inverse FFTs over p of the rows (set, t1), twiddle w_Nt^{-t1 n2}, out to W[n2][t1][pair]
+  fft_io<NP, 2 * N1, true, true, NTH, true, false, kRX>(
+      sm, s_twp,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(NP, kRX);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) v[m] = sm[pad(c * NP + j + m * s)];
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(NP, kRX);
+        const int set = c / N1, t1 = c % N1;
+        if (set == 1 && nsets == 1) return;  // the partner set is the same residue
+        const double2 tw = (set ? s_twb : s_twa)[t1];
+        double2* q = W + ((long long)(set ? n2p : n2) * N1 + t1) * Pc + pl0 + j;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) __stcg(q + m * s, cmul(w[m], tw));
+      });
+}
+
 template <int NT, int NX>
 void set_attrs() {
   using F = Fx<NT, NX>;
@@ -229,6 +427,8 @@ void set_attrs() {
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, false, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tfx_fwd_s2<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   cudaFuncSetAttribute(tfx_inv_s1<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_fwd_s2x<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_inv_s1x<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 1, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, false, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
@@ -253,7 +453,10 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
       tf4_fwd_s1<NT, N2, KP, true, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
     else
       tf4_fwd_s1<NT, N2, KP, false, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
-    tfx_fwd_s2<NT, NX><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, Sh, twx);
+    if (PD_TFX_XFIRST_FWD)
+      tfx_fwd_s2x<NT, NX><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, Sh, twx);
+    else
+      tfx_fwd_s2<NT, NX><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, Sh, twx);
     n += 2;
   }
   *nl = n;
@@ -274,7 +477,10 @@ cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, c
   for (long long p = 0; p < npairs; p += chunk_pairs) {
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
     const dim3 g1((unsigned)(pc / NP), N2 / 2 + 1), g2((unsigned)((pc + KP - 1) / KP), kN1);
-    tfx_inv_s1<NT, NX><<<g1, F::NTH, sm2, st>>>(Sh, S, p, pc, scratch, twx, tb.twt);
+    if (PD_TFX_XFIRST_INV)
+      tfx_inv_s1x<NT, NX><<<g1, F::NTH, sm2, st>>>(Sh, S, p, pc, scratch, twx, tb.twt);
+    else
+      tfx_inv_s1<NT, NX><<<g1, F::NTH, sm2, st>>>(Sh, S, p, pc, scratch, twx, tb.twt);
     const int th = KP * N2 / kRS;
     if (vec) {
       if (accumulate)
