@@ -169,6 +169,33 @@ PD_D void pass_twiddles(double2* v, int j, const double2* tw) {
   }
 }
 
+// Stockham-ordered twiddle table (N - 1 entries): pass p (stride LS, radix R) owns the entries
+// LS - 1 + (m - 1) LS + k = w_N^{m k N / (LS R)},  m = 1..R-1, k < LS,
+// so the lanes of a pass (consecutive k) read consecutive entries for every m.  A plain N-point table read
+// at the strides m k N/(LS R) is up to 8-way bank conflicted (m = 8 in the last pass of N = 256).
+struct TwStockham {
+  const double2* p;
+};
+template <int N, int R, int LS, bool INV>
+PD_D void pass_twiddles(double2* v, int j, TwStockham tw) {
+  if constexpr (LS > 1) {
+    const double2* t = tw.p + (LS - 1) + (j & (LS - 1));
+#pragma unroll
+    for (int m = 1; m < R; ++m) v[m] = cmul(v[m], twiddle<INV>(t, (m - 1) * LS));
+  }
+}
+// fill a TwStockham table for N-point FFTs with radix cap RMAX (all threads; caller synchronises);
+// w(idx) returns the forward twiddle w_N^idx
+template <int N, int RMAX, int P = 1, class WF>
+PD_D void build_stockham_table(double2* dst, WF w) {
+  if constexpr (P < num_passes(N, RMAX)) {  // pass 0 has no twiddles: its entries stay unused
+    constexpr int LS = ls_of(N, P, RMAX), R = radix_of(N, P, RMAX);
+    for (int i = threadIdx.x; i < (R - 1) * LS; i += blockDim.x)
+      dst[LS - 1 + i] = w((i / LS + 1) * (i % LS) * (N / (LS * R)));
+    build_stockham_table<N, RMAX, P + 1>(dst, w);
+  }
+}
+
 // read the R inputs (positions j + m*N/R) of butterfly (c, j) from smem
 template <int N, int C, int R, bool SEQMAJOR>
 PD_D void smem_read_bfly(const double2* sm, int j, int c, double2* v) {
@@ -185,8 +212,8 @@ PD_D void smem_write_out(double2* sm, int base, int c, const double2* v) {
 }
 
 // One Stockham radix-R pass smem -> smem over C sequences (all NTH threads participate).
-template <int N, int C, int R, int LS, bool INV, bool SEQMAJOR, int NTH>
-PD_D void stockham_pass(double2* sm, const double2* tw) {
+template <int N, int C, int R, int LS, bool INV, bool SEQMAJOR, int NTH, class TW>
+PD_D void stockham_pass(double2* sm, TW tw) {
   constexpr int NB = C * N / R;
   constexpr int BPT = NB / NTH;
   static_assert(BPT * NTH == NB, "butterflies must divide evenly");
@@ -213,7 +240,8 @@ PD_D void stockham_pass(double2* sm, const double2* tw) {
 // Passes P0..P1-1 (smem -> smem), compile-time recursion.
 template <int N, int C, int P, int P1, bool INV, bool SEQMAJOR, int NTH, int RMAX = 16>
 struct Passes {
-  static PD_D void run(double2* sm, const double2* tw) {
+  template <class TW>
+  static PD_D void run(double2* sm, TW tw) {
     if constexpr (P < P1) {
       stockham_pass<N, C, radix_of(N, P, RMAX), ls_of(N, P, RMAX), INV, SEQMAJOR, NTH>(sm, tw);
       Passes<N, C, P + 1, P1, INV, SEQMAJOR, NTH, RMAX>::run(sm, tw);
@@ -222,8 +250,8 @@ struct Passes {
 };
 
 // Full in-smem FFT of C sequences (natural order in, natural order out).
-template <int N, int C, bool INV, bool SEQMAJOR, int NTH>
-PD_D void fft_smem(double2* sm, const double2* tw) {
+template <int N, int C, bool INV, bool SEQMAJOR, int NTH, class TW>
+PD_D void fft_smem(double2* sm, TW tw) {
   Passes<N, C, 0, num_passes(N), INV, SEQMAJOR, NTH>::run(sm, tw);
 }
 
@@ -243,8 +271,8 @@ struct NoHook {
 // HOOK() runs (all threads) right after the barrier that follows pass 0's loads: the pipelined kernels use
 // it to recycle the stage buffer the loader just consumed.  RMAX: largest radix (16 or 8).
 template <int N, int C, bool INV, bool SEQMAJOR, int NTH, bool LOAD_SMEM, bool STORE_SMEM, int RMAX = 16, class LD,
-          class ST, class HOOK = NoHook>
-PD_D void fft_io(double2* sm, const double2* tw, LD ld, ST st, HOOK hook = HOOK()) {
+          class ST, class HOOK = NoHook, class TW = const double2*>
+PD_D void fft_io(double2* sm, TW tw, LD ld, ST st, HOOK hook = HOOK()) {
   constexpr int P = num_passes(N, RMAX);
   constexpr int R0 = radix_of(N, 0, RMAX);
   constexpr int B0 = (C * N / R0) / NTH;

@@ -253,18 +253,18 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(cons
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
   extern __shared__ double2 sm[];
-  __shared__ double2 s_twx[NP], s_twp[NP];
+  __shared__ double2 s_twx[NP], s_tws[NP - 1];
   const int n2 = blockIdx.y, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
   const long long pl0 = (long long)blockIdx.x * NP;
   const long long p0 = p_begin + pl0;
-  for (int i = threadIdx.x; i < NX; i += NTH) {
-    const double2 w = __ldg(twx + i);
-    if (i < NP) s_twx[i] = w;
-    if (!(i & 1)) s_twp[i >> 1] = w;
-  }
-  // (1) NP-point FFTs over p of the 2 N1 rows c = (set, t1) straight from Y[t1][n2][pair]
+  // (1) NP-point FFTs over p of the 2 N1 rows c = (set, t1) straight from Y[t1][n2][pair]; the twiddle
+  // tables are filled by the hook, after the tile loads are in flight (first used behind pass 0's barrier)
+  auto tables = [&] {
+    for (int i = threadIdx.x; i < NP; i += NTH) s_twx[i] = __ldg(twx + i);
+    build_stockham_table<NP, kRX>(s_tws, [&](int idx) { return __ldg(twx + 2 * idx); });
+  };
   fft_io<NP, 2 * N1, false, true, NTH, false, true, kRX>(
-      sm, s_twp,
+      sm, TwStockham{s_tws},
       [&](int j, auto st, int c, double2* v) {
         constexpr int s = decltype(st)::value, R0 = first_radix(NP, kRX);
         const int set = c / N1, t1 = c % N1;
@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(cons
         constexpr int s = decltype(st)::value, RL = last_radix(NP, kRX);
 #pragma unroll
         for (int m = 0; m < RL; ++m) sm[pad(c * NP + j + m * s)] = w[m];
-      });
+      },
+      tables);
   __syncthreads();
   // (2) N1-point DFTs over t1 of column k (set 0) and column NP - k (partner set), untangle, store
   const int sb = nsets == 2 ? 1 : 0;
@@ -329,22 +330,17 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(cons
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
   constexpr int NV = N1 / 2 + 1;  // rows n = r + N2 n1 <= Nt/2 have n1 <= N1/2
+  static_assert(NTH >= NP, "phase (0) runs one index k per thread");
   extern __shared__ double2 sm[];
-  __shared__ double2 s_twx[NP], s_twp[NP], s_twa[N1], s_twb[N1];
+  __shared__ double2 s_tws[NP - 1], s_twa[N1], s_twb[N1];
   const int n2 = blockIdx.y, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
   const int rb = nsets == 2 ? n2p : n2;  // residue of the partner set (self-partnered: the same set)
   const long long pl0 = (long long)blockIdx.x * NP;
   const long long p0 = p_begin + pl0;
-  for (int i = threadIdx.x; i < NX; i += NTH) {
-    const double2 w = __ldg(twx + i);
-    if (i < NP) s_twx[i] = w;
-    if (!(i & 1)) s_twp[i >> 1] = w;
-  }
-  if (threadIdx.x < N1) {
+  if (threadIdx.x < N1) {  // read behind the barrier that ends phase (0)
     s_twa[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2));
     s_twb[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2p));
   }
-  __syncthreads();
   // (0) per k: the stored rows n <= Nt/2 of set 0 at k and of the partner set at NP - k give every row of
   // set 0 at k and of the partner set at NP - k (direct or mirror); N1-point inverse DFTs over n1 -> smem
   for (int k = threadIdx.x; k < NP; k += NTH) {
@@ -364,7 +360,9 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(cons
         y1[n1] = __ldcs(q + NP);
       }
     }
-    const double2 wk = s_twx[k], wb = s_twx[kb];
+    const double2 wk = __ldg(twx + k), wb = __ldg(twx + kb);
+    // NTH >= NP: every thread that fills a table entry passes here exactly once
+    build_stockham_table<NP, kRX>(s_tws, [&](int idx) { return __ldg(twx + 2 * idx); });
     double2 a[N1];
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
@@ -397,7 +395,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(cons
   __syncthreads();
   // (1) NP-point inverse FFTs over p of the rows (set, t1), twiddle w_Nt^{-t1 n2}, out to W[n2][t1][pair]
   fft_io<NP, 2 * N1, true, true, NTH, true, false, kRX>(
-      sm, s_twp,
+      sm, TwStockham{s_tws},
       [&](int j, auto st, int c, double2* v) {
         constexpr int s = decltype(st)::value, R0 = first_radix(NP, kRX);
 #pragma unroll
