@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
                                                            const double* __restrict__ igam,
                                                            const double2* __restrict__ tw2) {
   constexpr int N1 = NT / N2, C = KP, NTH = KP * N2 / RM;
+  static_assert(num_passes(N2, RM) >= 2, "the hook-filled tables need pass 0's barrier");
   extern __shared__ double2 sm[];
   __shared__ double2 s_tw2[N2];
   __shared__ double s_g[N2];  // Gamma^{-1} / Nt of rows t1 + N1 t2
@@ -83,11 +84,12 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
   const long long pl0 = (long long)blockIdx.x * KP;
   const long long p0 = p_begin + pl0;
   const long long Pc = npairs_chunk;
-  for (int i = threadIdx.x; i < N2; i += NTH) {
-    s_tw2[i] = __ldg(tw2 + i);
-    s_g[i] = __ldg(igam + t1 + N1 * i) * (1.0 / NT);
-  }
-  __syncthreads();
+  auto tables = [&] {  // first read behind pass 0's barrier (twiddles) and in the storer (Gamma)
+    for (int i = threadIdx.x; i < N2; i += NTH) {
+      s_tw2[i] = __ldg(tw2 + i);
+      s_g[i] = __ldg(igam + t1 + N1 * i) * (1.0 / NT);
+    }
+  };
   const bool fullp = pl0 + KP <= Pc;
   fft_io<N2, C, true, false, NTH, false, false, RM>(
       sm, s_tw2,
@@ -145,7 +147,8 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
             }
           }
         }
-      });
+      },
+      tables);
 }
 
 template <int N>
