@@ -15,11 +15,15 @@ for rep in sys.argv[1:]:
         b = float(r[iR]) * scale[units[iR]] + float(r[iW]) * scale[units[iW]]
         per[r[iK].split("(")[0].replace("void ", "").strip()].append(b)
 big = {k: max(v) for k, v in per.items()}
-def get(prefix, pick=max):
-    ks = [k for k in per if k.startswith(prefix) or prefix in k]
-    return pick(per[ks[0]]) if ks else None
-fwd = 4 * (get("pdfft_tf4::tf4_fwd_s1<2048") + get("tfx_fwd_s2<2048"))
-inv = 4 * (get("tfx_inv_s1<2048") + get("pdfft_tf4::tf4_inv_s2<2048, 256, 16, 1, 0"))
+def get(*prefixes, pick=max):
+    for prefix in prefixes:  # first pattern present in the reports
+        ks = [k for k in per if k.startswith(prefix) or prefix in k]
+        if ks:
+            return pick(per[ks[0]])
+    return None
+# the x-first tfx kernels (default since r01 v11), else the t1-first ones
+fwd = 4 * (get("tf4_fwd_s1<2048") + get("tfx_fwd_s2x<2048", "tfx_fwd_s2<2048"))
+inv = 4 * (get("tfx_inv_s1x<2048", "tfx_inv_s1<2048") + get("tf4_inv_s2<2048, 256, 16, 1, 0"))
 cols = get("slab_ytri_kernel<512>") / 256 * 1025  # y-pass: per-slab bytes of a 256-slab chunk x F = 1025 slabs
 out = {"cfg4": {"tfft_fwd": fwd, "spatial_solve": cols, "tfft_inv": inv},
        "source": "ncu --set full --clock-control none, tools/prof_apply.py --config cfg4 (r01); per call = per-launch "
