@@ -350,6 +350,66 @@ PD_D double2 warp_affine_scan(double2 e, double2 M, double2* inc_last) {
 #ifndef PD_YTRI_C
 #define PD_YTRI_C 8  // columns (= warps) per CTA
 #endif
+#ifndef PD_YTRI_SPLIT
+#define PD_YTRI_SPLIT 1  // two interleaved half-length recurrence chains per lane (ILP 2 on the fp64 latency chains)
+#endif
+
+// One lane's L rows of a column, both recurrences, with each lane chunk split into halves A (rows 0..H-1) and
+// B (rows H..L-1), H = L/2, whose chains run interleaved:
+//   forward  a_j = r a_{j-1} + d_j,  b_j = r b_{j-1} + d_{H+j} (zero carry-ins); lane total r^H a_{H-1} + b_{H-1};
+//            with the lane carry-in q:  w_j = a_j + r^{j+1} q,  w_{H+j} = b_j + r^{j+1} (r^H q + a_{H-1})
+//   backward the mirror image from the top row down with s, -tau w and the carry from above
+// (the same sums as the single chain, regrouped).
+template <int L>
+PD_D void ytri_lane_split(double2* d, const pd_ytri_coef& cf, int lane, double scale) {
+  constexpr int H = L / 2;
+  double2 rH = cf.r, sH = cf.s;
+#pragma unroll
+  for (int h = 1; h < H; h <<= 1) {
+    rH = cmul(rH, rH);
+    sH = cmul(sH, sH);
+  }
+  double2 a = czero(), b = czero();
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    a = cfma(cf.r, a, d[j]);
+    d[j] = a;
+    b = cfma(cf.r, b, d[H + j]);
+    d[H + j] = b;
+  }
+  double2 tot;
+  const double2 cin = warp_affine_scan<false>(cfma(rH, a, b), cf.rL, &tot);
+  const double2 W = cmul(tot, cf.ir);
+  double2 qa = cfma(cpow_small(cf.rL, lane), W, cin);  // carry + r^{lane L} W
+  double2 qb = cfma(rH, qa, a);
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    qa = cmul(cf.r, qa);
+    d[j] = cadd(d[j], qa);
+    qb = cmul(cf.r, qb);
+    d[H + j] = cadd(d[H + j], qb);
+  }
+  const double2 mtau = cneg(cf.tau);
+  double2 u = czero(), l = czero();
+#pragma unroll
+  for (int jj = 0; jj < H; ++jj) {
+    u = cfma(cf.s, u, cmul(mtau, d[L - 1 - jj]));
+    d[L - 1 - jj] = u;
+    l = cfma(cf.s, l, cmul(mtau, d[H - 1 - jj]));
+    d[H - 1 - jj] = l;
+  }
+  const double2 cr = warp_affine_scan<true>(cfma(sH, u, l), cf.sL, &tot);
+  const double2 x0 = cmul(tot, cf.is);
+  double2 qu = cfma(cpow_small(cf.sL, 31 - lane), x0, cr);  // carry from above the lane
+  double2 ql = cfma(sH, qu, u);
+#pragma unroll
+  for (int jj = 0; jj < H; ++jj) {
+    qu = cmul(cf.s, qu);
+    d[L - 1 - jj] = cscale(cadd(d[L - 1 - jj], qu), scale);
+    ql = cmul(cf.s, ql);
+    d[H - 1 - jj] = cscale(cadd(d[H - 1 - jj], ql), scale);
+  }
+}
 #ifndef PD_YTRI_MINB
 #define PD_YTRI_MINB 0  // 0: by N (3 / 2 / 1)
 #endif
@@ -364,6 +424,8 @@ __global__ void __launch_bounds__(32 * kYC, PD_YTRI_MINB ? PD_YTRI_MINB : (N <= 
   const int n = slab0 + blockIdx.y;
   const int c0 = blockIdx.x * kYC;
   double2* slab = Sh + (long long)n * N * N + c0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const pd_ytri_coef cf = coef[(long long)(fglob0 + blockIdx.y) * N + c0 + w];  // in flight with the tile
   {
     // all N/32 loads of a thread in flight before the first smem store
     constexpr int PT = N / 32;
@@ -380,12 +442,13 @@ __global__ void __launch_bounds__(32 * kYC, PD_YTRI_MINB ? PD_YTRI_MINB : (N <= 
     }
   }
   __syncthreads();
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const pd_ytri_coef cf = coef[(long long)(fglob0 + blockIdx.y) * N + c0 + w];
   double2* col = sm + w * CS + lane * (L + 1);  // rows lane*L .. lane*L + L - 1 (+ one pad per lane chunk)
   double2 d[L];
 #pragma unroll
   for (int j = 0; j < L; ++j) d[j] = col[j];
+  if constexpr (PD_YTRI_SPLIT && L >= 4) {
+    ytri_lane_split<L>(d, cf, lane, scale);
+  } else {
   // forward: w'_i = r w'_{i-1} + d_i (zero carry-in), lane carries by scan, closure W = w_{N-1}
   double2 p = czero();
 #pragma unroll
@@ -417,6 +480,7 @@ __global__ void __launch_bounds__(32 * kYC, PD_YTRI_MINB ? PD_YTRI_MINB : (N <= 
   for (int j = L - 1; j >= 0; --j) {
     q = cmul(cf.s, q);
     d[j] = cscale(cadd(d[j], q), scale);
+  }
   }
 #pragma unroll
   for (int j = 0; j < L; ++j) col[j] = d[j];
