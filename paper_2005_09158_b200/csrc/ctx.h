@@ -67,6 +67,9 @@ struct pd_ctx {
   double2* tw_n1 = nullptr;      // four-step tables (Nt >= 1024)
   double2* tw_n2 = nullptr;
   double2* tf4_scratch = nullptr;
+  // PD_TF4_OVERLAP: second scratch chunk + stream for the two-stream four-step pipeline (tfx path)
+  bool use_ov = false;
+  pd_tfx_overlap ov{};
   long long tf4_chunk = 0;
   bool use_tf4 = false;
   bool use_tfx = false;           // 2D: four-step time FFT with the x-FFT folded in (tfx.cu)

@@ -53,12 +53,22 @@ cudaError_t pd_launch_tail1d(const double* g, double* part, int G, int nx, int n
 int pd_tfx_supported(int nt, int nx);
 int pd_tfx_n2(int nt);
 long long pd_tfx_chunk_align(int nt, int nx);
+// K-stream chunk pipeline (ov != nullptr, PD_TF4_OVERLAP=K): chunk i runs on stream i mod K with scratch
+// i mod K (stream 0 / scratch 0 = the caller's), so the stages of consecutive chunks overlap (same-stream order
+// protects each scratch); ev_fork orders the extra streams after st on entry, ev_join[k] st after them on exit.
+constexpr int kPdMaxOverlap = 4;
+struct pd_tfx_overlap {
+  int k = 1;
+  double2* scratch[kPdMaxOverlap] = {};
+  cudaStream_t st[kPdMaxOverlap] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kPdMaxOverlap] = {};
+};
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              cudaStream_t st, int* nl);
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);
 cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              int accumulate, cudaStream_t st, int* nl);
+                              int accumulate, cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);
 
 // ---- Step (b), 2D periodic: per-frequency slab 2D FFT -> divide -> inverse 2D FFT (slab2d.cu) ----
 // denominators lambda1_n + lambda2_n kappa(kx, ky), kappa = kd*(sx[kx]+sx[ky]) + i*(ax sn[kx] + ay sn[ky])/h

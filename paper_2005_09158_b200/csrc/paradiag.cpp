@@ -185,6 +185,12 @@ static void free_ctx(pd_ctx* c) {
   if (c->hred) cudaFreeHost(c->hred);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  for (int k = 1; k < kPdMaxOverlap; ++k) {
+    if (c->ov.scratch[k]) cudaFree(c->ov.scratch[k]);
+    if (c->ov.st[k]) cudaStreamDestroy(c->ov.st[k]);
+    if (c->ov.ev_join[k]) cudaEventDestroy(c->ov.ev_join[k]);
+  }
+  if (c->ov.ev_fork) cudaEventDestroy(c->ov.ev_fork);
   pd_dist_free(c);
   for (auto& e : c->evpool)
     if (e) cudaEventDestroy(e);
@@ -447,15 +453,28 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     SETUP_CUDA(cudaMemcpy(c->tw_n1, h1.data(), n1 * sizeof(double2), cudaMemcpyHostToDevice));
     SETUP_CUDA(cudaMemcpy(c->tw_n2, h2.data(), n2 * sizeof(double2), cudaMemcpyHostToDevice));
     const long long npairs = (c->S + 1) / 2;
-    // column chunk of the stage-1 -> stage-2 scratch (default 1 GB: launch count beats L2 residency, §5);
-    // 2D: whole x-rows
+    // column chunk of the stage-1 -> stage-2 scratch; 2D: whole x-rows.  One stream: 1 GB chunks (launch
+    // ramp/tail beats L2 residency, §5).  2D (tfx) default: 3 streams of 16 MB chunks (PD_TF4_OVERLAP = 3),
+    // so consecutive chunks' stages overlap and the scratch round trip mostly stays in L2 (§5)
+    const char* ov_env = getenv("PD_TF4_OVERLAP");
+    const int kov = c->use_tfx ? std::min(std::max(ov_env ? atoi(ov_env) : 3, 1), kPdMaxOverlap) : 1;
     const char* mb_env = getenv("PD_TF4_CHUNK_MB");
-    const long long mb = mb_env ? atoll(mb_env) : 1024;
+    const long long mb = mb_env ? atoll(mb_env) : (kov > 1 ? 16 : 1024);
     long long chunk = ((mb << 20) / ((long long)nt * 16)) / align * align;
     if (chunk < align) chunk = align;
     if (chunk > npairs) chunk = (npairs + align - 1) / align * align;
     c->tf4_chunk = chunk;
     SETUP_CUDA(dalloc(&c->tf4_scratch, (size_t)nt * chunk));
+    c->use_ov = kov > 1;
+    if (c->use_ov) {
+      c->ov.k = kov;
+      SETUP_CUDA(cudaEventCreateWithFlags(&c->ov.ev_fork, cudaEventDisableTiming));
+      for (int k = 1; k < kov; ++k) {
+        SETUP_CUDA(dalloc(&c->ov.scratch[k], (size_t)nt * chunk));
+        SETUP_CUDA(cudaStreamCreateWithFlags(&c->ov.st[k], cudaStreamNonBlocking));
+        SETUP_CUDA(cudaEventCreateWithFlags(&c->ov.ev_join[k], cudaEventDisableTiming));
+      }
+    }
   }
 
   // ---- workspace ----
@@ -605,7 +624,8 @@ pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) 
   phase_begin(c, 0);
   if (c->use_tfx) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, Sh, S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
+    PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, Sh, S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
+                                 c->use_ov ? &c->ov : nullptr));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
@@ -626,7 +646,7 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
   if (c->use_tfx) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tfx_inv(c->nt, c->g.nx, Sh, z, S, c->igam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
-                                 accumulate, c->st, &nl));
+                                 accumulate, c->st, &nl, c->use_ov ? &c->ov : nullptr));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;

@@ -434,9 +434,27 @@ void set_attrs() {
   done = dev;
 }
 
+// fork / join of the optional second stream (pd_tfx_overlap)
+inline cudaError_t ov_fork(const pd_tfx_overlap* ov, cudaStream_t st) {
+  if (!ov) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(ov->ev_fork, st);
+  for (int k = 1; k < ov->k && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ov->st[k], ov->ev_fork, 0);
+  return e;
+}
+inline cudaError_t ov_join(const pd_tfx_overlap* ov, cudaStream_t st) {
+  if (!ov) return cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  for (int k = 1; k < ov->k && e == cudaSuccess; ++k) {
+    e = cudaEventRecord(ov->ev_join[k], ov->st[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ov->ev_join[k], 0);
+  }
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 template <int NT, int NX>
 cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
-                const double2* twx, double2* scratch, long long chunk_pairs, cudaStream_t st, int* nl) {
+                const double2* twx, double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl,
+                const pd_tfx_overlap* ov) {
   using F = Fx<NT, NX>;
   constexpr int N2 = F::N2, KP = F::KP, NP = F::NP;
   set_attrs<NT, NX>();
@@ -444,7 +462,11 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
   const bool vec = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
   const long long npairs = S / 2;
   int n = 0;
-  for (long long p = 0; p < npairs; p += chunk_pairs) {
+  if (cudaError_t e = ov_fork(ov, st0)) return e;
+  for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
+    const int lane = ov ? (int)(ci % ov->k) : 0;
+    cudaStream_t st = lane ? ov->st[lane] : st0;
+    double2* scratch = lane ? ov->scratch[lane] : scratch0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
     const dim3 g1((unsigned)((pc + KP - 1) / KP), kN1), g2((unsigned)(pc / NP), N2 / 2 + 1);
     if (vec)
@@ -458,13 +480,13 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
     n += 2;
   }
   *nl = n;
-  return cudaGetLastError();
+  return ov_join(ov, st0);
 }
 
 template <int NT, int NX>
 cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
-                const double2* twx, double2* scratch, long long chunk_pairs, int accumulate, cudaStream_t st,
-                int* nl) {
+                const double2* twx, double2* scratch0, long long chunk_pairs, int accumulate, cudaStream_t st0,
+                int* nl, const pd_tfx_overlap* ov) {
   using F = Fx<NT, NX>;
   constexpr int N2 = F::N2, KP = F::KP, NP = F::NP;
   set_attrs<NT, NX>();
@@ -472,7 +494,11 @@ cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, c
   const bool vec = (reinterpret_cast<uintptr_t>(z) & 15) == 0;
   const long long npairs = S / 2;
   int n = 0;
-  for (long long p = 0; p < npairs; p += chunk_pairs) {
+  if (cudaError_t e = ov_fork(ov, st0)) return e;
+  for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
+    const int lane = ov ? (int)(ci % ov->k) : 0;
+    cudaStream_t st = lane ? ov->st[lane] : st0;
+    double2* scratch = lane ? ov->scratch[lane] : scratch0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
     const dim3 g1((unsigned)(pc / NP), N2 / 2 + 1), g2((unsigned)((pc + KP - 1) / KP), kN1);
     if (PD_TFX_XFIRST_INV)
@@ -494,15 +520,16 @@ cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, c
     n += 2;
   }
   *nl = n;
-  return cudaGetLastError();
+  return ov_join(ov, st0);
 }
 
 }  // namespace
 
-// Nt <= 512: the single-tile time FFT plus the three-launch slab solve measured faster on B200 (cfg3)
+// Nt <= 512: the single-tile time FFT plus the three-launch slab solve measured faster on B200 (cfg3).
+// NX = 1024 (instantiated, not parity-tested: Nt >= 1024 makes it 1e9 dofs) takes the tf4 + slab route.
 int pd_tfx_supported(int nt, int nx) {
   const bool t = nt == 1024 || nt == 2048 || nt == 4096;
-  const bool x = nx == 32 || nx == 64 || nx == 128 || nx == 256 || nx == 512 || nx == 1024;
+  const bool x = nx == 32 || nx == 64 || nx == 128 || nx == 256 || nx == 512;
   return t && x;
 }
 int pd_tfx_n2(int nt) { return nt / kN1; }
@@ -527,12 +554,12 @@ long long pd_tfx_chunk_align(int nt, int nx) {
 
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              cudaStream_t st, int* nl) {
-  PD_TFX_SWITCH(fwd, (r, Sh, S, gam, tb, twx, scratch, chunk_pairs, st, nl))
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov) {
+  PD_TFX_SWITCH(fwd, (r, Sh, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov))
 }
 
 cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              int accumulate, cudaStream_t st, int* nl) {
-  PD_TFX_SWITCH(inv, (Sh, z, S, igam, tb, twx, scratch, chunk_pairs, accumulate, st, nl))
+                              int accumulate, cudaStream_t st, int* nl, const pd_tfx_overlap* ov) {
+  PD_TFX_SWITCH(inv, (Sh, z, S, igam, tb, twx, scratch, chunk_pairs, accumulate, st, nl, ov))
 }

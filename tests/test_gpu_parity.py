@@ -36,6 +36,8 @@ SMALL = [
     (W.ADE2D, W.BE, 256, 4), (W.ADE2D, W.CN, 512, 2),
     # time FFT with the x-FFT folded in (tfx.cu, Nt >= 1024): several x-rows per chunk, both residue cases
     (W.ADE2D, W.BE, 32, 1024), (W.ADE2D, W.CN, 64, 1024), (W.ADE2D, W.CN, 32, 4096),
+    # every x-FFT pass plan of the x-first kernels: NP = 64 (16, 4), 128 (16, 8); NX = 1024 via the slab route
+    (W.ADE2D, W.CN, 128, 1024), (W.ADE2D, W.BE, 256, 1024), (W.ADE2D, W.BE, 1024, 2),
     # 2D homogeneous Dirichlet (Table T4A operator): tensor DST-I via odd-extension FFTs, ragged column tiles
     (W.WAVE2D, W.LF, 15, 16), (W.WAVE2D, W.LF, 31, 64), (W.WAVE2D, W.LF, 63, 1024), (W.WAVE2D, W.BE, 31, 8),
     (W.WAVE2D, W.LF, 255, 4),
