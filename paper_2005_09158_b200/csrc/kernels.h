@@ -18,12 +18,13 @@ struct pd_tf4_tables {
 int pd_tf4_supported(int nt);
 int pd_tf4_n2();
 int pd_tf4_pairs_per_tile();
+struct pd_tfx_overlap;  // optional K-stream chunk pipeline (below)
 cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
-                              int* nl);
+                              int* nl, const pd_tfx_overlap* ov = nullptr);
 cudaError_t pd_launch_tf4_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, int accumulate,
-                              cudaStream_t st, int* nl);
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);
 
 // ---- Step (b), 1D: batched constant-coefficient complex tridiagonal solves (tridiag.cu) ----
 // Per frequency n (row n of Sh, nx entries): (a_n x_{i-1} + b_n x_i + c_n x_{i+1}) = d_i with
@@ -63,6 +64,22 @@ struct pd_tfx_overlap {
   cudaStream_t st[kPdMaxOverlap] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kPdMaxOverlap] = {};
 };
+// fork (extra streams wait for st) / join (st waits for the extra streams); no-ops without ov
+inline cudaError_t ov_fork(const pd_tfx_overlap* ov, cudaStream_t st) {
+  if (!ov) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(ov->ev_fork, st);
+  for (int k = 1; k < ov->k && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ov->st[k], ov->ev_fork, 0);
+  return e;
+}
+inline cudaError_t ov_join(const pd_tfx_overlap* ov, cudaStream_t st) {
+  if (!ov) return cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  for (int k = 1; k < ov->k && e == cudaSuccess; ++k) {
+    e = cudaEventRecord(ov->ev_join[k], ov->st[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ov->ev_join[k], 0);
+  }
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);

@@ -454,10 +454,10 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     SETUP_CUDA(cudaMemcpy(c->tw_n2, h2.data(), n2 * sizeof(double2), cudaMemcpyHostToDevice));
     const long long npairs = (c->S + 1) / 2;
     // column chunk of the stage-1 -> stage-2 scratch; 2D: whole x-rows.  One stream: 1 GB chunks (launch
-    // ramp/tail beats L2 residency, §5).  2D (tfx) default: 3 streams of 16 MB chunks (PD_TF4_OVERLAP = 3),
-    // so consecutive chunks' stages overlap and the scratch round trip mostly stays in L2 (§5)
+    // ramp/tail beats L2 residency, §5).  Default: 3 streams of 16 MB chunks (PD_TF4_OVERLAP = 3), so
+    // consecutive chunks' stages overlap and the scratch round trip mostly stays in L2 (§5)
     const char* ov_env = getenv("PD_TF4_OVERLAP");
-    const int kov = c->use_tfx ? std::min(std::max(ov_env ? atoi(ov_env) : 3, 1), kPdMaxOverlap) : 1;
+    const int kov = std::min(std::max(ov_env ? atoi(ov_env) : 3, 1), kPdMaxOverlap);
     const char* mb_env = getenv("PD_TF4_CHUNK_MB");
     const long long mb = mb_env ? atoll(mb_env) : (kov > 1 ? 16 : 1024);
     long long chunk = ((mb << 20) / ((long long)nt * 16)) / align * align;
@@ -629,7 +629,8 @@ pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) 
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, Sh, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl));
+    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, Sh, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
+                                 c->use_ov ? &c->ov : nullptr));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, Sh, S, c->gam, c->tw_t, c->st));
@@ -650,7 +651,8 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl));
+    PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl,
+                                 c->use_ov ? &c->ov : nullptr));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, Sh, z, S, c->igam, c->tw_t, accumulate, c->st));

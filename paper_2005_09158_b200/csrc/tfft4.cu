@@ -236,34 +236,42 @@ void inv_grid(const double2* Sh, double* z, long long S, const double* igam, con
 
 constexpr int kRmaxGrid = 8;  // radix-8 passes: 8 elements per thread, twice the warps of radix 16 (measured faster)
 
+// chunk ci of a call: stream / scratch ci mod K of the optional pipeline (kernels.h pd_tfx_overlap)
 template <int NT>
 cudaError_t fwd_n(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
-                  double2* scratch, long long chunk_pairs, cudaStream_t st, int* nl) {
+                  double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl, const pd_tfx_overlap* ov) {
   const bool vec = (S % 2 == 0) && ((reinterpret_cast<uintptr_t>(r) & 15) == 0);
   const long long npairs = (S + 1) / 2;
   int n = 0;
-  for (long long p = 0; p < npairs; p += chunk_pairs) {
+  if (cudaError_t e = ov_fork(ov, st0)) return e;
+  for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
+    const int lane = ov ? (int)(ci % ov->k) : 0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
-    fwd_grid<NT, kRmaxGrid>(r, Sh, S, gam, tb, scratch, p, pc, vec, st);
+    fwd_grid<NT, kRmaxGrid>(r, Sh, S, gam, tb, lane ? ov->scratch[lane] : scratch0, p, pc, vec,
+                            lane ? ov->st[lane] : st0);
     n += 2;
   }
   *nl = n;
-  return cudaGetLastError();
+  return ov_join(ov, st0);
 }
 
 template <int NT>
 cudaError_t inv_n(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
-                  double2* scratch, long long chunk_pairs, int accumulate, cudaStream_t st, int* nl) {
+                  double2* scratch0, long long chunk_pairs, int accumulate, cudaStream_t st0, int* nl,
+                  const pd_tfx_overlap* ov) {
   const bool vec = (S % 2 == 0) && ((reinterpret_cast<uintptr_t>(z) & 15) == 0);
   const long long npairs = (S + 1) / 2;
   int n = 0;
-  for (long long p = 0; p < npairs; p += chunk_pairs) {
+  if (cudaError_t e = ov_fork(ov, st0)) return e;
+  for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
+    const int lane = ov ? (int)(ci % ov->k) : 0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
-    inv_grid<NT, kRmaxGrid>(Sh, z, S, igam, tb, scratch, p, pc, accumulate, vec, st);
+    inv_grid<NT, kRmaxGrid>(Sh, z, S, igam, tb, lane ? ov->scratch[lane] : scratch0, p, pc, accumulate, vec,
+                            lane ? ov->st[lane] : st0);
     n += 2;
   }
   *nl = n;
-  return cudaGetLastError();
+  return ov_join(ov, st0);
 }
 
 }  // namespace
@@ -274,24 +282,24 @@ int pd_tf4_pairs_per_tile() { return kP; }
 
 cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
-                              int* nl) {
+                              int* nl, const pd_tfx_overlap* ov) {
   switch (nt) {
-    case 1024: return fwd_n<1024>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
-    case 2048: return fwd_n<2048>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
-    case 4096: return fwd_n<4096>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
-    case 8192: return fwd_n<8192>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl);
+    case 1024: return fwd_n<1024>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 2048: return fwd_n<2048>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 4096: return fwd_n<4096>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 8192: return fwd_n<8192>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t pd_launch_tf4_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, int accumulate,
-                              cudaStream_t st, int* nl) {
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov) {
   switch (nt) {
-    case 1024: return inv_n<1024>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
-    case 2048: return inv_n<2048>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
-    case 4096: return inv_n<4096>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
-    case 8192: return inv_n<8192>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl);
+    case 1024: return inv_n<1024>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 2048: return inv_n<2048>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 4096: return inv_n<4096>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 8192: return inv_n<8192>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -434,23 +434,6 @@ void set_attrs() {
   done = dev;
 }
 
-// fork / join of the optional second stream (pd_tfx_overlap)
-inline cudaError_t ov_fork(const pd_tfx_overlap* ov, cudaStream_t st) {
-  if (!ov) return cudaSuccess;
-  cudaError_t e = cudaEventRecord(ov->ev_fork, st);
-  for (int k = 1; k < ov->k && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ov->st[k], ov->ev_fork, 0);
-  return e;
-}
-inline cudaError_t ov_join(const pd_tfx_overlap* ov, cudaStream_t st) {
-  if (!ov) return cudaGetLastError();
-  cudaError_t e = cudaSuccess;
-  for (int k = 1; k < ov->k && e == cudaSuccess; ++k) {
-    e = cudaEventRecord(ov->ev_join[k], ov->st[k]);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ov->ev_join[k], 0);
-  }
-  return e == cudaSuccess ? cudaGetLastError() : e;
-}
-
 template <int NT, int NX>
 cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
                 const double2* twx, double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl,
