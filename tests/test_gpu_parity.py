@@ -68,6 +68,19 @@ def test_apply_matches_oracle_small(op, scheme, nx, nt):
     check_apply(cfg, r, z)
 
 
+@pytest.mark.parametrize("kov,mb", [(1, 1024), (1, 8), (2, 8), (4, 4)])
+@pytest.mark.parametrize("op,scheme,nx,nt", [(W.ADE2D, W.CN, 64, 1024), (W.ADE1D, W.BE, 2047, 4096)])
+def test_apply_time_fft_pipeline_variants(monkeypatch, op, scheme, nx, nt, kov, mb):
+    """The four-step time FFT's chunk pipeline (default 3 streams of 16 MB): one stream of large or
+    small chunks and 2 / 4 streams of many small chunks give the oracle's apply (env read at context setup)."""
+    monkeypatch.setenv("PD_TF4_OVERLAP", str(kov))
+    monkeypatch.setenv("PD_TF4_CHUNK_MB", str(mb))
+    cfg = _cfg(op, scheme, nx, nt, alpha=0.02)
+    r = W.random_vector(cfg, seed=nx + kov * 13 + mb)
+    z = to_host(make_ctx(cfg).apply_precond(to_dev(r)))
+    check_apply(cfg, r, z)
+
+
 @pytest.mark.parametrize("alpha", [1.0, 0.5, 1e-4])
 def test_apply_alpha_range(alpha):
     cfg = _cfg(W.ADE1D, W.CN, 129, 64, alpha=alpha)
