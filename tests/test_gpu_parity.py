@@ -81,6 +81,26 @@ def test_apply_time_fft_pipeline_variants(monkeypatch, op, scheme, nx, nt, kov, 
     check_apply(cfg, r, z)
 
 
+@pytest.mark.parametrize("op,scheme,nx,nt", [(W.ADE2D, W.CN, 64, 1024), (W.ADE1D, W.CN, 1023, 1024)])
+def test_apply_graph_replay(monkeypatch, op, scheme, nx, nt):
+    """PD_GRAPH=1: the first apply of an (r, z) pair is captured (with the time-FFT stream pipeline's fork/join
+    as parallel branches) and every later one replays the graph; the replays see new contents of r."""
+    import torch
+    monkeypatch.setenv("PD_GRAPH", "1")
+    cfg = _cfg(op, scheme, nx, nt, alpha=0.02)
+    ctx = make_ctx(cfg)
+    r1, r2 = W.random_vector(cfg, seed=1), W.random_vector(cfg, seed=2)
+    rd = to_dev(r1)
+    zd = torch.empty_like(rd)
+    ctx.apply_precond(rd, zd)            # capture + launch
+    check_apply(cfg, r1, to_host(zd))
+    ctx.apply_precond(rd, zd)            # replay
+    check_apply(cfg, r1, to_host(zd))
+    rd.copy_(to_dev(r2))
+    ctx.apply_precond(rd, zd)            # replay on new data
+    check_apply(cfg, r2, to_host(zd))
+
+
 @pytest.mark.parametrize("alpha", [1.0, 0.5, 1e-4])
 def test_apply_alpha_range(alpha):
     cfg = _cfg(W.ADE1D, W.CN, 129, 64, alpha=alpha)
