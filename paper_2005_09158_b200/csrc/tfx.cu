@@ -52,6 +52,9 @@ constexpr int kRX = PD_TFX_RM;
 #ifndef PD_TFX_XFIRST_INV
 #define PD_TFX_XFIRST_INV PD_TFX_XFIRST
 #endif
+#ifndef PD_TFX_KPT
+#define PD_TFX_KPT 4096  // elements of a stage-1 tile (N2 x KP pairs)
+#endif
 constexpr int kRS = PD_TFX_S1_RM;
 
 template <int NT, int NX>
@@ -59,7 +62,7 @@ struct Fx {
   static constexpr int N1 = kN1, N2 = NT / kN1, NP = NX / 2, C = 2 * NP, NTH = 8 * NX / kRX;
   static constexpr int ROWS = 2 * N1;                 // rows (n1, set) of NP values
   static constexpr int SMEM = smem_elems(ROWS * NP);  // complex elements
-  static constexpr int KP = 4096 / N2 < 8 ? 8 : 4096 / N2;  // stage-1 pairs per tile (N2 * KP = 4096)
+  static constexpr int KP = PD_TFX_KPT / N2 < 8 ? 8 : PD_TFX_KPT / N2;  // stage-1 pairs per tile (N2 * KP = KPT)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -517,7 +520,7 @@ int pd_tfx_supported(int nt, int nx) {
 }
 int pd_tfx_n2(int nt) { return nt / kN1; }
 long long pd_tfx_chunk_align(int nt, int nx) {
-  const long long kp = 4096 / (nt / kN1) < 8 ? 8 : 4096 / (nt / kN1);
+  const long long kp = PD_TFX_KPT / (nt / kN1) < 8 ? 8 : PD_TFX_KPT / (nt / kN1);
   const long long np = nx / 2;
   return kp > np ? kp : np;
 }
