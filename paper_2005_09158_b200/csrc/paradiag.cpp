@@ -1021,9 +1021,16 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     if (s != PD_OK) return s;
     s = pd_apply_impl(c, c->zvec, u, 1);
     if (s != PD_OK) return s;
-    s = pd_stencil_impl(c, b, u, c->V[0], &rr);  // true residual, also the restart vector X_0
-    Xv[0] = c->V[0];
+    // true residual norm; the residual vector (the restart vector X_0) is written only when a restart follows
+    // (single GPU: the norm-only stencil writes nothing)
+    const bool norm_only = c->dist_mode == 0;
+    s = pd_stencil_impl(c, b, u, norm_only ? nullptr : c->V[0], &rr);
     if (s != PD_OK) return s;
+    if (norm_only && !(std::sqrt(rr) <= tol * bnorm) && its < maxit && !breakdown) {
+      s = pd_stencil_impl(c, b, u, c->V[0], &rr);
+      if (s != PD_OK) return s;
+    }
+    Xv[0] = c->V[0];
     beta = std::sqrt(rr);
     conv = beta <= tol * bnorm;
     if (breakdown) break;

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kBX, 4) stencil1d_kernel(pd_stencil p, const d
     if (act) {
       const long long idx = (long long)n * nx + x;
       const double v = b ? b[idx] - Au : Au;
-      out[idx] = v;
+      if (out) out[idx] = v;  // out == NULL: norm only
       acc = fma(v, v, acc);
     }
     h2 = h1;
@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
   if (ldR) { R.h1 = ld(pc - rstride, n0 - 1, dr); if (NT == 3) R.h2 = ld(pc - 2 * rstride, n0 - 2, dr); }
   const long long off = (long long)n0 * S + (long long)y * nx + x;
   const double* pb = b ? b + off : nullptr;
-  double* po = out + off;
+  const bool wr = out != nullptr;  // NULL: norm only (no vector written)
+  double* po = wr ? out + off : nullptr;
   // one-row prefetch
   double nc = live ? pc[0] : 0.0, nl = ldL ? pc[dl] : 0.0, nr = ldR ? pc[dr] : 0.0;
   double nb = (act && pb) ? pb[0] : 0.0;
@@ -226,10 +227,10 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
       double Au = comb1<NT>(p, c);
       Au += p.k2c * yc + p.k2x_m * yxm + p.k2x_p * yxp + p.k2y_m * yym + p.k2y_p * yyp;
       const double v = pb ? bv - Au : Au;
-      *po = v;
+      if (wr) *po = v;
       acc = fma(v, v, acc);
     }
-    po += S;
+    if (wr) po += S;
     if (pb) pb += S;
     c.h2 = c.h1; c.h1 = c.h0;
     L.h2 = L.h1; L.h1 = L.h0;

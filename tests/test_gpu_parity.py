@@ -227,6 +227,26 @@ def test_solver_variants_match_oracle(name, solver):
     assert rel(u, u_ref) < SOLVE_TOL
 
 
+@pytest.mark.parametrize("name,m", [("cfg1", 2), ("cfg3", 3)])
+def test_gmres_restarts_match_oracle(name, m):
+    """Restarted GMRES(m) with m far below the unrestarted count: every cycle ends with the true residual (a
+    norm-only sweep, then the restart vector written only when a restart follows) and the counts, residual
+    histories and solutions stay the oracle's."""
+    cfg = W.BY_NAME[name]
+    if name == "cfg3":
+        cfg = cfg.scaled(nx=64, ny=64, nt=64)
+    ctx = make_ctx(cfg)
+    f = W.source_samples(cfg)
+    b_dev = ctx.build_rhs(to_dev(W.initial_u0(cfg)), to_dev(W.initial_v0(cfg)), None if f is None else to_dev(f))
+    b = to_host(b_dev)
+    u_gpu, rep = ctx.solve_gmres(b_dev, tol=cfg.tol, m=m, maxit=200)
+    u_ref, rep_ref = solvers.solve_gmres(cfg, b, tol=cfg.tol, m=m, maxit=200)
+    assert rep.converged and rep_ref.converged
+    assert rep.iterations == rep_ref.iterations > m, (rep.iterations, rep_ref.iterations)
+    assert rel(to_host(u_gpu), u_ref) < SOLVE_TOL
+    assert rep.rel_residual <= cfg.tol
+
+
 def test_cfg4_solve_reduced_scale_matches_oracle():
     """Config 4 recipe at 1/32 of the dofs (N=128, Nt=1024): same operator, alpha, scheme, tolerance, m."""
     cfg = W.BY_NAME["cfg4"].scaled(nx=128, ny=128, nt=1024)
