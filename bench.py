@@ -81,27 +81,40 @@ def cpu_baseline(cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md recipe)."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md recipe).
+
+    nvidia-smi is started before the region (it needs a few hundred ms to come up) and samples every 20 ms with its
+    own timestamps; only samples inside [begin(), end()] (host wall clock) are kept, so a short region still gets
+    its own samples.  If none falls inside, the nearest ones are reported and flagged."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.8)
         except Exception:
             self.proc = None
         return self
 
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *a):
         self.lines = []
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
@@ -111,21 +124,36 @@ class ClockSampler:
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+        rows = []
         for ln in getattr(self, "lines", []):
             f = [x.strip() for x in ln.split(",")]
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[1]), float(f[2]), f[4:8]))
             except (ValueError, IndexError):
                 continue
-            for name, v in zip(names, f[3:7]):
+        if not rows:
+            return None
+        inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        flag = None
+        if not inside:
+            mid = 0.5 * (self.t0 + self.t1) if self.t0 is not None else rows[-1][0]
+            inside = sorted(rows, key=lambda r: abs(r[0] - mid))[:3]
+            flag = "no sample inside the timed region: the nearest 3"
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for _, smv, mxv, rs in inside:
+            sm.append(smv)
+            mx = mxv
+            for name, v in zip(names, rs):
                 if v.lower().startswith("active"):
                     reasons.add(name)
-        if not sm:
-            return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if flag:
+            out["note"] = flag
+        return out
+
 
 
 def main():
@@ -192,6 +220,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        clk.begin()
         e0.record(stream)
         its = []
         for _ in range(args.steps):
@@ -199,6 +228,7 @@ def main():
             its.append(rep.iterations)
         e1.record(stream)
         barrier()
+        clk.end()
     ms = e0.elapsed_time(e1) / args.steps
     launches = ctx.kernel_launches() - launches0
     pms, pn = ctx.phase_times()
