@@ -19,6 +19,14 @@ int pd_tf4_supported(int nt);
 int pd_tf4_n2();
 int pd_tf4_pairs_per_tile();
 struct pd_tfx_overlap;  // optional K-stream chunk pipeline (below)
+// Linear combination sum_i c[i] x[i] of k <= kPdCombMax device vectors (16-byte aligned, S even) read by the
+// forward time FFT's stage-1 loader in place of r (the GMRES final update u += P^{-1} (V y), tfx path).
+constexpr int kPdCombMax = 32;
+struct pd_comb_args {
+  const double* x[kPdCombMax];
+  double c[kPdCombMax];
+  int k;
+};
 cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
                               int* nl, const pd_tfx_overlap* ov = nullptr);
@@ -82,7 +90,8 @@ inline cudaError_t ov_join(const pd_tfx_overlap* ov, cudaStream_t st) {
 }
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr,
+                              const pd_comb_args* comb = nullptr);  // comb: r unused
 cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               int accumulate, cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);

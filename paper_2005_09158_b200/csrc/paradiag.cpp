@@ -670,6 +670,22 @@ static pd_status apply_direct(pd_ctx* c, const double* r, double* z, int accumul
   return pd_time_fft_inv(c, c->Sh, z, c->S, accumulate);
 }
 
+// u += P^{-1} (sum_i cb.c[i] cb.x[i]) with the combination read by the forward time FFT's stage-1 loader (tfx path,
+// single GPU; the GMRES final update).  The fused forward is timed with the Krylov sweeps (phase 6): it is the
+// combination sweep plus a time FFT, so it does not enter the per-call average of the forward time FFT.
+static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double* u) {
+  const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
+  phase_begin(c, 6);
+  int nl = 0;
+  PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, nullptr, c->Sh, c->S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
+                               c->st, &nl, c->use_ov ? &c->ov : nullptr, cb));
+  c->launches += nl;
+  phase_end(c, 6);
+  pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
+  if (s != PD_OK) return s;
+  return pd_time_fft_inv(c, c->Sh, u, c->S, 1);
+}
+
 // z = P^{-1} r, or u += P^{-1} r when accumulate.  With graphs enabled (single GPU, phase timing off) the
 // launch sequence of each (r, z, accumulate) triple is captured once and replayed as one CUDA graph.
 pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
@@ -1017,10 +1033,25 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
       y[i] = t / Hs(i, i);
     }
     for (int i = 0; i < kk; ++i) coef[i] = y[i] * sc[i];
-    s = krylov_impl(c, 3, Xp, coef.data(), kk, 0.0, c->zvec, nullptr);
-    if (s != PD_OK) return s;
-    s = pd_apply_impl(c, c->zvec, u, 1);
-    if (s != PD_OK) return s;
+    // fused: the forward time FFT reads the basis combination itself (tfx path, single GPU, no graphs)
+    bool fused = c->use_tfx && c->dist_mode == 0 && !c->use_graphs && kk <= kPdCombMax && c->S % 2 == 0 &&
+                 getenv("PD_GMRES_NO_FUSED_UPDATE") == nullptr;
+    pd_comb_args cb{};
+    for (int i = 0; fused && i < kk; ++i) {
+      fused = (reinterpret_cast<uintptr_t>(Xp[i]) & 15) == 0;
+      cb.x[i] = Xp[i];
+      cb.c[i] = coef[i];
+    }
+    cb.k = kk;
+    if (fused) {
+      s = apply_comb_accumulate(c, &cb, u);
+      if (s != PD_OK) return s;
+    } else {
+      s = krylov_impl(c, 3, Xp, coef.data(), kk, 0.0, c->zvec, nullptr);
+      if (s != PD_OK) return s;
+      s = pd_apply_impl(c, c->zvec, u, 1);
+      if (s != PD_OK) return s;
+    }
     // true residual norm; the residual vector (the restart vector X_0) is written only when a restart follows
     // (single GPU: the norm-only stencil writes nothing)
     const bool norm_only = c->dist_mode == 0;

@@ -66,6 +66,66 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restr
       });
 }
 
+// Forward stage 1 reading r = sum_k cb.c[k] cb.x[k] (pd_comb_args, 16-byte aligned vectors, S even): the
+// combination of the GMRES final update fused into the time FFT (one read of each basis vector instead of a
+// combination sweep that writes r and a stage 1 that reads it back).  Otherwise identical to tf4_fwd_s1<VEC>.
+template <int NT, int N2, int KP, int RM = 16>
+__global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1_comb(const __grid_constant__ pd_comb_args cb, long long S,
+                                                                long long p_begin, long long npairs_chunk,
+                                                                double2* __restrict__ Y,
+                                                                const double* __restrict__ gam,
+                                                                const double2* __restrict__ tw2,
+                                                                const double2* __restrict__ twt) {
+  constexpr int N1 = NT / N2, C = KP, NTH = KP * N2 / RM;
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw2[N2], s_twr[N2];
+  __shared__ double s_g[N2];
+  const int t1 = blockIdx.y;
+  const long long pl0 = (long long)blockIdx.x * KP;
+  const long long p0 = p_begin + pl0;
+  const long long Pc = npairs_chunk;
+  for (int i = threadIdx.x; i < N2; i += NTH) {
+    s_tw2[i] = __ldg(tw2 + i);
+    s_twr[i] = __ldg(twt + t1 * i);
+    s_g[i] = __ldg(gam + t1 + N1 * i);
+  }
+  __syncthreads();
+  const bool fullp = pl0 + KP <= Pc;
+  fft_io<N2, C, false, false, NTH, false, false, RM>(
+      sm, s_tw2,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value, R0 = first_radix(N2, RM);
+        const long long off = (long long)(t1 + N1 * j) * S + 2 * (p0 + c);
+        const long long step = (long long)N1 * s * S;
+        double2 acc[R0];
+#pragma unroll
+        for (int m = 0; m < R0; ++m) acc[m] = czero();
+        if (fullp || pl0 + c < Pc) {
+          for (int k = 0; k < cb.k; ++k) {
+            const double ck = cb.c[k];
+            const double* q = cb.x[k] + off;
+            double2 t[R0];
+#pragma unroll
+            for (int m = 0; m < R0; ++m) t[m] = __ldcs(reinterpret_cast<const double2*>(q + m * step));
+#pragma unroll
+            for (int m = 0; m < R0; ++m) acc[m] = make_double2(fma(ck, t[m].x, acc[m].x), fma(ck, t[m].y, acc[m].y));
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < R0; ++m) {
+          const double g = s_g[j + m * s];
+          v[m] = make_double2(g * acc[m].x, g * acc[m].y);
+        }
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value, RL = last_radix(N2, RM);
+        if (!(fullp || pl0 + c < Pc)) return;
+        double2* q = Y + ((long long)t1 * N2 + j) * Pc + pl0 + c;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) __stcg(q + (long long)m * s * Pc, cmul(w[m], s_twr[j + m * s]));
+      });
+}
+
 // ---------------------------------------------------------------------------------------------
 // inverse stage 2: for fixed t1 (blockIdx.y): N2-point inverse FFT over n2 of W[n2][t1][.], outputs
 // t = t1 + N1 t2 scaled by Gamma^{-1}_t / Nt into the two real columns of each pair (MODE 1: +=).

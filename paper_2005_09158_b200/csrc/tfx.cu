@@ -426,6 +426,7 @@ void set_attrs() {
   const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, true, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, false, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tf4_fwd_s1_comb<NT, N2, KP, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tfx_fwd_s2<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   cudaFuncSetAttribute(tfx_inv_s1<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   cudaFuncSetAttribute(tfx_fwd_s2x<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -440,7 +441,7 @@ void set_attrs() {
 template <int NT, int NX>
 cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
                 const double2* twx, double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl,
-                const pd_tfx_overlap* ov) {
+                const pd_tfx_overlap* ov, const pd_comb_args* comb) {
   using F = Fx<NT, NX>;
   constexpr int N2 = F::N2, KP = F::KP, NP = F::NP;
   set_attrs<NT, NX>();
@@ -455,7 +456,9 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
     double2* scratch = lane ? ov->scratch[lane] : scratch0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
     const dim3 g1((unsigned)((pc + KP - 1) / KP), kN1), g2((unsigned)(pc / NP), N2 / 2 + 1);
-    if (vec)
+    if (comb)
+      tf4_fwd_s1_comb<NT, N2, KP, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(*comb, S, p, pc, scratch, gam, tb.tw2, tb.twt);
+    else if (vec)
       tf4_fwd_s1<NT, N2, KP, true, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
     else
       tf4_fwd_s1<NT, N2, KP, false, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
@@ -540,8 +543,8 @@ long long pd_tfx_chunk_align(int nt, int nx) {
 
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov) {
-  PD_TFX_SWITCH(fwd, (r, Sh, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov))
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov, const pd_comb_args* comb) {
+  PD_TFX_SWITCH(fwd, (r, Sh, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov, comb))
 }
 
 cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,

@@ -247,6 +247,26 @@ def test_gmres_restarts_match_oracle(name, m):
     assert rep.rel_residual <= cfg.tol
 
 
+def test_gmres_fused_final_update_equals_unfused(monkeypatch):
+    """The GMRES final update u += P^{-1}(V y) with the combination read by the time FFT's stage-1 loader (fused,
+    the tfx default) equals the combination sweep + apply (PD_GMRES_NO_FUSED_UPDATE=1), and the oracle."""
+    cfg = W.BY_NAME["cfg4"].scaled(nx=64, ny=64, nt=1024)
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("PD_GMRES_NO_FUSED_UPDATE", env)
+        ctx = make_ctx(cfg)
+        b = ctx.build_rhs(to_dev(W.initial_u0(cfg)))
+        u, rep = ctx.solve_gmres(b, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
+        outs.append((to_host(u), rep))
+        bh = to_host(b)
+    (u1, r1), (u2, r2) = outs
+    assert r1.converged and r2.converged and r1.iterations == r2.iterations
+    assert rel(u1, u2) < 1e-12
+    u_ref, rep_ref = solvers.solve_gmres(cfg, bh)
+    assert r1.iterations == rep_ref.iterations and rel(u1, u_ref) < SOLVE_TOL
+
+
 def test_cfg4_solve_reduced_scale_matches_oracle():
     """Config 4 recipe at 1/32 of the dofs (N=128, Nt=1024): same operator, alpha, scheme, tolerance, m."""
     cfg = W.BY_NAME["cfg4"].scaled(nx=128, ny=128, nt=1024)
