@@ -95,9 +95,10 @@ typedef struct {
  * forms DESIGN.md §3), Gamma tables, twiddles; allocate the workspace; check every shifted system for
  * singularity.  alpha in (0,1]; Nt a power of two (>= 2, >= 4 for PD_LEAPFROG); dt > 0.
  * cuda_stream: a cudaStream_t (NULL = legacy default stream).  dist may be NULL (single GPU).
- * For Nt >= 1024 the context also owns two internal non-blocking streams and their scratch chunks (the time-FFT
+ * For Nt >= 1024 the context also owns up to three internal non-blocking streams and their scratch chunks (the time-FFT
  * chunk pipeline); every call still behaves as if ordered on cuda_stream (event fork / join).
- * Tuning environment (read here, at setup): PD_TF4_OVERLAP (streams, default 3), PD_TF4_CHUNK_MB, PD_GRAPH.
+ * Tuning environment (read here, at setup): PD_TF4_OVERLAP / PD_TF4_OVERLAP_INV (streams of the forward /
+ * inverse time FFT, default 3 / 4), PD_TF4_CHUNK_MB, PD_GRAPH.
  * Returns PD_EINVAL / PD_ESINGULAR / PD_ENOMEM / PD_ECUDA / PD_ENCCL on failure (*out = NULL). */
 PD_API pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme s, const pd_dist* dist,
                    void* cuda_stream, pd_ctx** out);

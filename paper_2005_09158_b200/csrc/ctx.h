@@ -69,7 +69,8 @@ struct pd_ctx {
   double2* tf4_scratch = nullptr;
   // PD_TF4_OVERLAP: second scratch chunk + stream for the two-stream four-step pipeline (tfx path)
   bool use_ov = false;
-  pd_tfx_overlap ov{};
+  pd_tfx_overlap ov{};      // forward time FFT view (owns the streams / scratches / events, up to the larger count)
+  pd_tfx_overlap ov_inv{};  // inverse view of the same pool (its own stream count)
   long long tf4_chunk = 0;
   bool use_tf4 = false;
   bool use_tfx = false;           // 2D: four-step time FFT with the x-FFT folded in (tfx.cu)

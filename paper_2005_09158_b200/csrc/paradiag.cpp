@@ -458,22 +458,29 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     // consecutive chunks' stages overlap and the scratch round trip mostly stays in L2 (§5)
     const char* ov_env = getenv("PD_TF4_OVERLAP");
     const int kov = std::min(std::max(ov_env ? atoi(ov_env) : 3, 1), kPdMaxOverlap);
+    // the inverse measured best with 4 streams (2.84 vs 2.88 ms on cfg4), the forward with 3 (2.68 vs 2.75)
+    const char* ovi_env = getenv("PD_TF4_OVERLAP_INV");
+    const int kovi = std::min(std::max(ovi_env ? atoi(ovi_env) : (ov_env ? kov : 4), 1), kPdMaxOverlap);
+    const int kmax = std::max(kov, kovi);
     const char* mb_env = getenv("PD_TF4_CHUNK_MB");
-    const long long mb = mb_env ? atoll(mb_env) : (kov > 1 ? 16 : 1024);
+    const long long mb = mb_env ? atoll(mb_env) : (kmax > 1 ? 16 : 1024);
     long long chunk = ((mb << 20) / ((long long)nt * 16)) / align * align;
     if (chunk < align) chunk = align;
     if (chunk > npairs) chunk = (npairs + align - 1) / align * align;
     c->tf4_chunk = chunk;
     SETUP_CUDA(dalloc(&c->tf4_scratch, (size_t)nt * chunk));
-    c->use_ov = kov > 1;
+    c->use_ov = kmax > 1;
     if (c->use_ov) {
-      c->ov.k = kov;
+      c->ov.k = kmax;
       SETUP_CUDA(cudaEventCreateWithFlags(&c->ov.ev_fork, cudaEventDisableTiming));
-      for (int k = 1; k < kov; ++k) {
+      for (int k = 1; k < kmax; ++k) {
         SETUP_CUDA(dalloc(&c->ov.scratch[k], (size_t)nt * chunk));
         SETUP_CUDA(cudaStreamCreateWithFlags(&c->ov.st[k], cudaStreamNonBlocking));
         SETUP_CUDA(cudaEventCreateWithFlags(&c->ov.ev_join[k], cudaEventDisableTiming));
       }
+      c->ov_inv = c->ov;
+      c->ov.k = kov;
+      c->ov_inv.k = kovi;
     }
   }
 
@@ -625,12 +632,12 @@ pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) 
   if (c->use_tfx) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, Sh, S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
-                                 c->use_ov ? &c->ov : nullptr));
+                                 c->ov.k > 1 ? &c->ov : nullptr));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, Sh, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
-                                 c->use_ov ? &c->ov : nullptr));
+                                 c->ov.k > 1 ? &c->ov : nullptr));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, Sh, S, c->gam, c->tw_t, c->st));
@@ -647,12 +654,12 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
   if (c->use_tfx) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tfx_inv(c->nt, c->g.nx, Sh, z, S, c->igam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
-                                 accumulate, c->st, &nl, c->use_ov ? &c->ov : nullptr));
+                                 accumulate, c->st, &nl, c->ov_inv.k > 1 ? &c->ov_inv : nullptr));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl,
-                                 c->use_ov ? &c->ov : nullptr));
+                                 c->ov_inv.k > 1 ? &c->ov_inv : nullptr));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, Sh, z, S, c->igam, c->tw_t, accumulate, c->st));
@@ -678,7 +685,7 @@ static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double
   phase_begin(c, 6);
   int nl = 0;
   PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, nullptr, c->Sh, c->S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
-                               c->st, &nl, c->use_ov ? &c->ov : nullptr, cb));
+                               c->st, &nl, c->ov.k > 1 ? &c->ov : nullptr, cb));
   c->launches += nl;
   phase_end(c, 6);
   pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
