@@ -646,6 +646,13 @@ pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) 
   return PD_OK;
 }
 
+// stream pool view of the inverse time FFT: 4 streams for z = ..., the forward's 3 for the accumulating u += ...
+// (which also reads u: 4.02 vs 3.86 ms on cfg4 with 4 streams)
+static const pd_tfx_overlap* inv_view(const pd_ctx* c, int accumulate) {
+  const pd_tfx_overlap& v = accumulate ? c->ov : c->ov_inv;
+  return v.k > 1 ? &v : nullptr;
+}
+
 // Step (c) of a local slab: Sh [F][S] -> z [Nt][S] (z += when accumulate)
 pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate) {
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
@@ -654,12 +661,12 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
   if (c->use_tfx) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tfx_inv(c->nt, c->g.nx, Sh, z, S, c->igam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
-                                 accumulate, c->st, &nl, c->ov_inv.k > 1 ? &c->ov_inv : nullptr));
+                                 accumulate, c->st, &nl, inv_view(c, accumulate)));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
     PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl,
-                                 c->ov_inv.k > 1 ? &c->ov_inv : nullptr));
+                                 inv_view(c, accumulate)));
     c->launches += nl;
   } else {
     PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, Sh, z, S, c->igam, c->tw_t, accumulate, c->st));
