@@ -206,11 +206,11 @@ def main():
                       None if f is None else dev(np.ascontiguousarray(f[:, sl])))
     u = torch.zeros_like(b)
 
-    def step():
-        u.zero_()
+    def step():  # one full solve from u = 0 (GMRES: pd_solve with PD_SOLVE_ZERO_GUESS, u output only)
         if cfg.solver == "stationary":
+            u.zero_()
             return ctx.solve_stationary(b, u, tol=cfg.tol, maxit=cfg.maxit)[1]
-        return ctx.solve_gmres(b, u, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)[1]
+        return ctx.solve_gmres(b, u, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit, zero_guess=True)[1]
 
     for _ in range(args.warmup):
         rep = step()

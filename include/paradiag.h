@@ -140,6 +140,11 @@ PD_API pd_status pd_solve_stationary(pd_ctx* ctx, const double* b, double* u, do
 /* Right-preconditioned restarted GMRES(m), CGS2 orthogonalisation, deterministic reductions.
  * Workspace for the basis ((m+1) vectors) is allocated on first use and kept by the context. */
 PD_API pd_status pd_solve_gmres(pd_ctx* ctx, const double* b, double* u, double tol, int m, int maxit, pd_report* rep);
+/* Either solver with flags: solver 0 stationary, 1 GMRES, OR-ed with PD_SOLVE_ZERO_GUESS = start from u = 0 with u
+ * output only (not read, may hold anything on entry: GMRES then skips the zero-guess check sweep and writes the
+ * first cycle's update instead of adding it).  Otherwise identical to pd_solve_stationary / pd_solve_gmres. */
+PD_API pd_status pd_solve(pd_ctx* ctx, int solver, const double* b, double* u, double tol, int m, int maxit,
+                          pd_report* rep);
 
 /* ---- waveform-relaxation tail form (oracle/tail.py) ----
  * P_alpha - A is non-zero only between the first H time blocks (rows) and the last H blocks (columns),

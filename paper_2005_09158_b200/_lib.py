@@ -13,6 +13,7 @@ _HEADER = os.path.join(os.path.dirname(_HERE), "include", "paradiag.h")
 ADE1D_DIRICHLET, WAVE1D_DIRICHLET, ADE2D_PERIODIC, WAVE2D_DIRICHLET = 0, 1, 2, 3
 BE, CN, LEAPFROG = 0, 1, 2
 PD_OK, PD_NOT_CONVERGED = 0, 1
+SOLVE_ZERO_GUESS = 16  # include/paradiag.h PD_SOLVE_ZERO_GUESS
 _STATUS = {0: "PD_OK", 1: "PD_NOT_CONVERGED", -1: "PD_EINVAL", -2: "PD_ESINGULAR", -3: "PD_ECUDA",
            -4: "PD_ENCCL", -5: "PD_ENOMEM", -6: "PD_EBREAKDOWN"}
 
@@ -84,6 +85,7 @@ def load_library(path: str | None = None):
         "pd_solve_ivp_host": (ip, [vp, ip, vp, vp, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_apply_precond_host": (ip, [vp, vp, vp]),
         "pd_solve_host": (ip, [vp, ip, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
+        "pd_solve": (ip, [vp, ip, vp, vp, C.c_double, ip, ip, C.POINTER(pd_report)]),
         "pd_kernel_launches": (C.c_longlong, [vp]),
         "pd_enable_phase_timing": (ip, [vp, ip]),
         "pd_phase_times": (ip, [vp, dp, C.POINTER(C.c_longlong)]),
@@ -249,11 +251,17 @@ class ParaDiag:
             _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
         return u, self._mk(st, rep, hist)
 
-    def solve_gmres(self, b, u=None, tol=1e-10, m=20, maxit=100, raise_on_fail=True):
+    def solve_gmres(self, b, u=None, tol=1e-10, m=20, maxit=100, raise_on_fail=True, zero_guess=False):
+        """zero_guess: start from u = 0 with u output only (pd_solve with PD_SOLVE_ZERO_GUESS; u not read)."""
         import torch
-        u = torch.zeros(self.shape, dtype=torch.float64, device="cuda") if u is None else u
+        if u is None:
+            u = torch.empty(self.shape, dtype=torch.float64, device="cuda") if zero_guess else \
+                torch.zeros(self.shape, dtype=torch.float64, device="cuda")
         rep, hist = self._report(maxit + 2)
-        st = self._lib.pd_solve_gmres(self._ctx, _ptr(b), _ptr(u), tol, m, maxit, C.byref(rep))
+        if zero_guess:
+            st = self._lib.pd_solve(self._ctx, 1 | SOLVE_ZERO_GUESS, _ptr(b), _ptr(u), tol, m, maxit, C.byref(rep))
+        else:
+            st = self._lib.pd_solve_gmres(self._ctx, _ptr(b), _ptr(u), tol, m, maxit, C.byref(rep))
         if raise_on_fail:
             _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
         return u, self._mk(st, rep, hist)

@@ -687,7 +687,7 @@ static pd_status apply_direct(pd_ctx* c, const double* r, double* z, int accumul
 // u += P^{-1} (sum_i cb.c[i] cb.x[i]) with the combination read by the forward time FFT's stage-1 loader (tfx path,
 // single GPU; the GMRES final update).  The fused forward is timed with the Krylov sweeps (phase 6): it is the
 // combination sweep plus a time FFT, so it does not enter the per-call average of the forward time FFT.
-static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double* u) {
+static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double* u, int accumulate) {
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   phase_begin(c, 6);
   int nl = 0;
@@ -697,7 +697,7 @@ static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double
   phase_end(c, 6);
   pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
   if (s != PD_OK) return s;
-  return pd_time_fft_inv(c, c->Sh, u, c->S, 1);
+  return pd_time_fft_inv(c, c->Sh, u, c->S, accumulate);
 }
 
 // z = P^{-1} r, or u += P^{-1} r when accumulate.  With graphs enabled (single GPU, phase timing off) the
@@ -855,7 +855,9 @@ pd_status pd_solve_stationary(pd_ctx* c, const double* b, double* u, double tol,
   return conv ? PD_OK : PD_NOT_CONVERGED;
 }
 
-pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int m, int maxit, pd_report* rep) {
+// zero_guess: u is output only (not read; no zero-check sweep); otherwise u is the initial guess
+static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, int m, int maxit, pd_report* rep,
+                            bool zero_guess) {
   if (!c || !b || !u) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
   if (!(tol > 0) || maxit < 0 || m < 1 || m > 30) return fail(c, PD_EINVAL, "need tol > 0, maxit >= 0, 1 <= m <= 30");
   const auto t0 = std::chrono::steady_clock::now();
@@ -899,7 +901,11 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
   std::vector<const double*> Xv(c->V.begin(), c->V.end());
   double rr = 0;
   bool u_zero = false;
-  if (c->dist_mode == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {  // b read in place by the Krylov kernels
+  if (zero_guess && !(c->dist_mode == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0)) {
+    PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * n, c->st));  // b not usable in place: the general path
+  } else if (zero_guess) {
+    u_zero = true;
+  } else if (c->dist_mode == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {  // b read in place by the Krylov kernels
     if (!c->gm_flag) {
       PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->gm_flag), sizeof(int)));
       PD_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->gm_hflag), sizeof(int)));
@@ -937,6 +943,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     if (!c->gm_head) PD_CUDA(c, dalloc(&c->gm_head, (size_t)(2 * c->S + 2)));
     dhead = c->gm_head;
   }
+  bool u_is_zero = u_zero;  // until the first cycle's update: that update writes u instead of adding to it
   while (!conv && its < maxit) {
     sc[0] = 1.0 / beta;
     std::fill(gv.begin(), gv.end(), 0.0);
@@ -1057,13 +1064,15 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
       cb.c[i] = coef[i];
     }
     cb.k = kk;
+    const int acc = u_is_zero ? 0 : 1;  // u = 0: u + x == x exactly, so write x (no read of u)
+    u_is_zero = false;
     if (fused) {
-      s = apply_comb_accumulate(c, &cb, u);
+      s = apply_comb_accumulate(c, &cb, u, acc);
       if (s != PD_OK) return s;
     } else {
       s = krylov_impl(c, 3, Xp, coef.data(), kk, 0.0, c->zvec, nullptr);
       if (s != PD_OK) return s;
-      s = pd_apply_impl(c, c->zvec, u, 1);
+      s = pd_apply_impl(c, c->zvec, u, acc);
       if (s != PD_OK) return s;
     }
     // true residual norm; the residual vector (the restart vector X_0) is written only when a restart follows
@@ -1080,6 +1089,7 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
     conv = beta <= tol * bnorm;
     if (breakdown) break;
   }
+  if (u_is_zero && zero_guess) PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * n, c->st));  // no cycle ran
   if (rep) {
     rep->iterations = its;
     rep->converged = conv;
@@ -1089,6 +1099,20 @@ pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int 
   if (conv) return PD_OK;
   if (breakdown) return fail(c, PD_EBREAKDOWN, "GMRES breakdown at iteration %d, residual %.3e", its, beta / bnorm);
   return PD_NOT_CONVERGED;
+}
+
+pd_status pd_solve_gmres(pd_ctx* c, const double* b, double* u, double tol, int m, int maxit, pd_report* rep) {
+  return gmres_impl(c, b, u, tol, m, maxit, rep, false);
+}
+
+pd_status pd_solve(pd_ctx* c, int solver, const double* b, double* u, double tol, int m, int maxit, pd_report* rep) {
+  if (!c) return PD_EINVAL;
+  const bool zero = (solver & PD_SOLVE_ZERO_GUESS) != 0;
+  solver &= ~PD_SOLVE_ZERO_GUESS;
+  if (solver == 1) return gmres_impl(c, b, u, tol, m, maxit, rep, zero);
+  if (solver != 0) return fail(c, PD_EINVAL, "pd_solve: solver %d not in {0 stationary, 1 gmres}", solver);
+  if (zero && u) PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * c->nt * c->S, c->st));
+  return pd_solve_stationary(c, b, u, tol, maxit, rep);
 }
 
 // ---- host-buffer variants ----

@@ -267,6 +267,24 @@ def test_gmres_fused_final_update_equals_unfused(monkeypatch):
     assert r1.iterations == rep_ref.iterations and rel(u1, u_ref) < SOLVE_TOL
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg4s", "cfg3s"])
+def test_gmres_zero_guess_flag(name):
+    """pd_solve(GMRES | PD_SOLVE_ZERO_GUESS) with u full of NaN (so any read of it would show) gives the same
+    iterations and bit-identical solution as pd_solve_gmres from a zero-filled u, incl. restarts (m = 2) and a
+    right-hand side already converged at u = 0 (b = 0 is handled before; tol = 1e3)."""
+    import torch
+    cfg = {"cfg1": W.BY_NAME["cfg1"], "cfg4s": W.BY_NAME["cfg4"].scaled(nx=64, ny=64, nt=1024),
+           "cfg3s": W.BY_NAME["cfg3"].scaled(nx=64, ny=64, nt=64)}[name]
+    ctx = make_ctx(cfg)
+    b = ctx.build_rhs(to_dev(W.initial_u0(cfg)))
+    for m, tol in ((cfg.m, cfg.tol), (2, cfg.tol), (cfg.m, 1e3)):
+        u1, r1 = ctx.solve_gmres(b, tol=tol, m=m, maxit=100)
+        u2 = torch.full_like(b, float("nan"))
+        u2, r2 = ctx.solve_gmres(b, u2, tol=tol, m=m, maxit=100, zero_guess=True)
+        assert r1.converged and r2.converged and r1.iterations == r2.iterations
+        assert torch.equal(u1, u2), (m, tol)
+
+
 def test_cfg4_solve_reduced_scale_matches_oracle():
     """Config 4 recipe at 1/32 of the dofs (N=128, Nt=1024): same operator, alpha, scheme, tolerance, m."""
     cfg = W.BY_NAME["cfg4"].scaled(nx=128, ny=128, nt=1024)
