@@ -1143,13 +1143,14 @@ pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, dou
   if (s != PD_OK) return s;
   const size_t bytes = sizeof(double) * c->nt * c->S;
   PD_CUDA(c, cudaMemcpyAsync(c->stage_a, bh, bytes, cudaMemcpyHostToDevice, c->st));
-  if (solver & PD_SOLVE_ZERO_GUESS)
-    PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
-  else
-    PD_CUDA(c, cudaMemcpyAsync(c->stage_b, uh, bytes, cudaMemcpyHostToDevice, c->st));
+  const bool zero = (solver & PD_SOLVE_ZERO_GUESS) != 0;
   solver &= ~PD_SOLVE_ZERO_GUESS;
+  if (!zero)
+    PD_CUDA(c, cudaMemcpyAsync(c->stage_b, uh, bytes, cudaMemcpyHostToDevice, c->st));
+  else if (solver == 0)
+    PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
   s = solver == 0 ? pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep)
-                  : pd_solve_gmres(c, c->stage_a, c->stage_b, tol, m, maxit, rep);
+                  : gmres_impl(c, c->stage_a, c->stage_b, tol, m, maxit, rep, zero);
   if (s < 0) return s;
   PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
   PD_CUDA(c, cudaStreamSynchronize(c->st));
@@ -1175,10 +1176,11 @@ pd_status pd_solve_ivp_host(pd_ctx* c, int solver, const double* u0h, const doub
   }
   s = pd_build_rhs(c, du0, v0h ? dv0 : nullptr, df, c->stage_a);
   if (s != PD_OK) return s;
-  PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
+  // from u = 0: GMRES takes the zero-guess path (u output only), the others start from a zeroed u
+  if (solver != 1) PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
   switch (solver) {
     case 0: s = pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
-    case 1: s = pd_solve_gmres(c, c->stage_a, c->stage_b, tol, m, maxit, rep); break;
+    case 1: s = gmres_impl(c, c->stage_a, c->stage_b, tol, m, maxit, rep, true); break;
     case 2: s = pd_solve_stationary_tail(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
     case 3: s = pd_solve_gmres_tail(c, c->stage_a, c->stage_b, tol, m, maxit, rep); break;
     default: s = pd_solve_newton(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
