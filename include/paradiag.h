@@ -93,7 +93,8 @@ typedef struct {
 
 /* Create a context: validate, build the spectra lambda_{1,n}, lambda_{2,n} (Lemma 1, P:l.155-174; closed
  * forms DESIGN.md §3), Gamma tables, twiddles; allocate the workspace; check every shifted system for
- * singularity.  alpha in (0,1]; Nt a power of two (>= 2, >= 4 for PD_LEAPFROG); dt > 0.
+ * singularity.  alpha in (0,1]; Nt a power of two in [1, 8192] (>= 4 for PD_LEAPFROG; Nt = 1 is one plain solve
+ * (c1 I + c2 K) z = r, S:l.89, reading t2); dt > 0.
  * cuda_stream: a cudaStream_t (NULL = legacy default stream).  dist may be NULL (single GPU).
  * For Nt >= 1024 the context also owns up to three internal non-blocking streams and their scratch chunks (the time-FFT
  * chunk pipeline); every call still behaves as if ordered on cuda_stream (event fork / join).
@@ -152,9 +153,11 @@ PD_API pd_status pd_solve(pd_ctx* ctx, int solver, const double* b, double* u, d
  * carry only the "tail" of u between iterations (head-tail coupling of WR, P:l.762-773; economical Step (a),
  * P:l.928-931).  Same iterates, iteration counts and stopping rule (||b - A u|| <= tol ||b||) as the
  * residual-form solvers above; per iteration the work is the tail map below plus O(H S) vector operations
- * instead of full passes over Nt x S.  Single-GPU contexts only (dist == NULL or size 1): PD_EINVAL otherwise;
- * PD_EINVAL also when Nt < 2H.  Per-context tables (1D: F x H coefficients; 2D: the N x N transfer function
- * tau, F N^2 divisions) are built on the first call and kept.
+ * instead of full passes over Nt x S.  Sharded contexts (NCCL or virtual ranks) replicate the H head / tail blocks
+ * on every rank: the 1D tail map splits its frequencies over the ranks and all-reduces the H x S tail, the 2D one
+ * runs replicated (tailform.cpp).  PD_EINVAL when Nt < 2H and for PD_WAVE2D_DIRICHLET (no tail map).  Per-context
+ * tables (1D: F x H coefficients; 2D: the N x N transfer function tau, F N^2 divisions) are built on the first call
+ * and kept.
  *
  * pd_tail_map: tail = last H blocks of P_alpha^{-1} (E_H head), head and tail device [H][local dofs]
  *   (must not alias).  Economical Step (a), Step (b) for every frequency, last H rows of Step (c). */
@@ -179,9 +182,12 @@ PD_API pd_status pd_set_reaction(pd_ctx* ctx, double g3, double g1);
 PD_API pd_status pd_solve_newton(pd_ctx* ctx, const double* b, double* u, double tol, int maxit, pd_report* rep);
 
 /* HOST-buffer variants for end-to-end use: copy the HOST input(s) to device workspace on the context
- * stream (pinned memory recommended), run, copy the HOST output back, synchronise.
+ * stream (pinned memory recommended), run, copy the HOST output back, synchronise.  Every HOST vector holds
+ * exactly Nt * (local spatial dofs) doubles (pd_local_size); the library cannot check host extents, so a shorter
+ * buffer is an out-of-bounds access (the Python binding checks dtype, device, contiguity and element count).
  * pd_solve_host: solver 0 stationary, 1 GMRES; OR-ing PD_SOLVE_ZERO_GUESS starts from u = 0 without copying
- * u_host in (u_host is then output only: one host->device copy per solve instead of two). */
+ * u_host in (u_host is then output only: one host->device copy per solve instead of two).  Any other solver code
+ * is PD_EINVAL. */
 #define PD_SOLVE_ZERO_GUESS 16
 PD_API pd_status pd_apply_precond_host(pd_ctx* ctx, const double* r_host, double* z_host);
 PD_API pd_status pd_solve_host(pd_ctx* ctx, int solver /*0 stationary, 1 gmres*/, const double* b_host,

@@ -91,20 +91,30 @@ def apply_precond_dense(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
     return _lf_dense(cfg, r, alpha, K)
 
 
-def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.ndarray:
+def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None, precision=np.float64) -> np.ndarray:
     """Same as apply_precond_dense, in the eigenbasis of K (scalar recurrences per mode).
 
     WAVE1D: K = Q diag(mu) Q^T with the DST-I basis Q_{jk} = sqrt(2/(N+1)) sin(pi j k/(N+1)),
             mu_k = (4/h^2) sin^2(pi k / (2(N+1)))  (textbook eigenpairs of the Dirichlet -D2).
     ADE2D : K = F^{-1} diag(kappa) F with the 2D DFT (symbol: reading c14).
+    precision: np.float64, or np.longdouble (WAVE1D / WAVE2D only) for the extended-precision references of
+    readings t1 and x4 (the same steps in x87 80-bit arithmetic; the 2x2 head-tail systems by Cramer's rule).
     """
     alpha = cfg.alpha if alpha is None else alpha
     nt, dt = r.shape[0], cfg.dt
+    ext = np.dtype(precision) != np.float64
+    cdt = np.result_type(precision, np.complex64)
+    if ext and cfg.op not in (WAVE1D, WAVE2D):
+        raise ValueError("extended precision: WAVE1D / WAVE2D only")
+    pi = 4 * np.arctan(np.asarray(1, dtype=precision)) if ext else math.pi
+    if ext:
+        r = np.asarray(r, dtype=precision)
+        dt = precision(1) * cfg.T / nt
     if cfg.op == WAVE1D:
         n, h = cfg.nx, cfg.h
-        j = np.arange(1, n + 1)
-        Q = math.sqrt(2.0 / (n + 1)) * np.sin(math.pi * np.outer(j, j) / (n + 1))
-        mu = (4.0 / h ** 2) * np.sin(math.pi * j / (2 * (n + 1))) ** 2
+        j = np.arange(1, n + 1, dtype=precision)
+        Q = np.sqrt(precision(2) / (n + 1)) * np.sin(pi * np.outer(j, j) / (n + 1))
+        mu = (4 / precision(h) ** 2) * np.sin(pi * j / (2 * (n + 1))) ** 2
         rh = r @ Q                      # modal coefficients (Q symmetric orthogonal)
         to_nodal = lambda zh: zh @ Q
     elif cfg.op == ADE2D:
@@ -116,9 +126,9 @@ def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
         to_nodal = lambda zh: ((Fi @ zh.reshape(nt, n, n) @ Fi.T) / (n * n)).real.reshape(nt, n * n)
     elif cfg.op == WAVE2D:  # tensor DST-I basis, mu_{kl} = mu_k + mu_l
         n, h = cfg.nx, cfg.h
-        j = np.arange(1, n + 1)
-        Q = math.sqrt(2.0 / (n + 1)) * np.sin(math.pi * np.outer(j, j) / (n + 1))
-        m1 = (4.0 / h ** 2) * np.sin(math.pi * j / (2 * (n + 1))) ** 2
+        j = np.arange(1, n + 1, dtype=precision)
+        Q = np.sqrt(precision(2) / (n + 1)) * np.sin(pi * np.outer(j, j) / (n + 1))
+        m1 = (4 / precision(h) ** 2) * np.sin(pi * j / (2 * (n + 1))) ** 2
         mu = (m1[:, None] + m1[None, :]).reshape(-1)
         rh = (Q @ r.reshape(nt, n, n) @ Q).reshape(nt, n * n)
         to_nodal = lambda zh: (Q @ zh.reshape(nt, n, n) @ Q).reshape(nt, n * n)
@@ -131,14 +141,14 @@ def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
         g = (1.0 / dt - (1.0 - th) * mu) / l
 
         def sweep(z0):
-            z = np.empty((nt, mu.size), dtype=np.complex128)
+            z = np.empty((nt, mu.size), dtype=cdt)
             prev = z0
             for k in range(nt):
                 prev = g * prev + rh[k] / l
                 z[k] = prev
             return z
 
-        y = sweep(np.zeros(mu.size, dtype=np.complex128))
+        y = sweep(np.zeros(mu.size, dtype=cdt))
         w = y[-1] / (1.0 - alpha * g ** nt)
         zh = sweep(alpha * w)
     else:
@@ -147,7 +157,7 @@ def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
         c_b = (2.0 / dt ** 2) / l                # coefficient of z_k
 
         def sweep(zm1, z0):
-            z = np.empty((nt, mu.size), dtype=np.complex128)
+            z = np.empty((nt, mu.size), dtype=cdt)
             a, b = zm1, z0
             for k in range(nt):
                 c = c_a * a + c_b * b + rh[k] / l
@@ -155,14 +165,14 @@ def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
                 a, b = b, c
             return z
 
-        zero = np.zeros(mu.size, dtype=np.complex128)
+        zero = np.zeros(mu.size, dtype=cdt)
         y = sweep(zero, zero)
         # per-mode 2x2 propagator G = [[0, 1], [c_a, c_b]] raised to Nt
-        G = np.zeros((mu.size, 2, 2), dtype=np.complex128)
+        G = np.zeros((mu.size, 2, 2), dtype=cdt)
         G[:, 0, 1] = 1.0
         G[:, 1, 0] = c_a
         G[:, 1, 1] = c_b
-        Gn = np.broadcast_to(np.eye(2, dtype=np.complex128), G.shape).copy()
+        Gn = np.broadcast_to(np.eye(2, dtype=cdt), G.shape).copy()
         P, e = G.copy(), nt
         while e:
             if e & 1:
@@ -172,7 +182,12 @@ def apply_precond_modal(cfg, r: np.ndarray, alpha: float | None = None) -> np.nd
                 P = P @ P
         Mtx = np.broadcast_to(np.eye(2), G.shape) - alpha * Gn
         rhs = np.stack([y[-2], y[-1]], axis=-1)[..., None]
-        w = np.linalg.solve(Mtx, rhs)[..., 0]
+        if ext:  # LAPACK has no extended precision: Cramer's rule on the 2x2 systems
+            det = Mtx[:, 0, 0] * Mtx[:, 1, 1] - Mtx[:, 0, 1] * Mtx[:, 1, 0]
+            w = np.stack([(Mtx[:, 1, 1] * y[-2] - Mtx[:, 0, 1] * y[-1]) / det,
+                          (Mtx[:, 0, 0] * y[-1] - Mtx[:, 1, 0] * y[-2]) / det], axis=-1)
+        else:
+            w = np.linalg.solve(Mtx, rhs)[..., 0]
         zh = sweep(alpha * w[:, 0], alpha * w[:, 1])
     z = to_nodal(zh)
     return np.real(z) if np.iscomplexobj(z) else z

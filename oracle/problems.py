@@ -75,8 +75,16 @@ def K_matrix(cfg) -> sp.csr_matrix:
 
 
 def apply_K(cfg, U: np.ndarray) -> np.ndarray:
-    """K applied to every time block of U [Nt][S] (or a single block [S])."""
+    """K applied to every time block of U [Nt][S] (or a single block [S]).
+
+    Extended-precision U (np.longdouble; scipy.sparse has no such dtype) takes the row sums of the same CSR
+    entries in U's precision: (K U)_i = sum_j K_ij U_j."""
     K = K_matrix(cfg)
+    if U.dtype == np.longdouble:
+        Ut = U.reshape(-1, K.shape[0]).T                                   # [S][blocks]
+        prod = K.data.astype(np.longdouble)[:, None] * Ut[K.indices]      # one row per stored entry
+        out = np.add.reduceat(prod, K.indptr[:-1], axis=0).T              # every row of K has entries
+        return np.ascontiguousarray(out).reshape(U.shape)
     if U.ndim == 1:
         return K @ U
     return np.ascontiguousarray((K @ U.T).T)

@@ -74,9 +74,9 @@ def solve_gmres(cfg, b, u0=None, tol=None, m=None, maxit=None, apply=None):
         return u, Report(0, True, beta / bnorm, hist)
     while True:
         V = [r.reshape(-1) / beta]
-        H = np.zeros((m + 1, m))
-        cs, sn = np.zeros(m), np.zeros(m)
-        g = np.zeros(m + 1)
+        H = np.zeros((m + 1, m), dtype=b.dtype)   # b.dtype: float64, or np.longdouble for reading x4's reference
+        cs, sn = np.zeros(m, dtype=b.dtype), np.zeros(m, dtype=b.dtype)
+        g = np.zeros(m + 1, dtype=b.dtype)
         g[0] = beta
         k = 0
         breakdown = False
@@ -107,7 +107,7 @@ def solve_gmres(cfg, b, u0=None, tol=None, m=None, maxit=None, apply=None):
                 breakdown = True
                 break
             V.append(w / hnext)
-        y = np.zeros(k)
+        y = np.zeros(k, dtype=b.dtype)
         for i in range(k - 1, -1, -1):
             y[i] = (g[i] - np.dot(H[i, i + 1:k], y[i + 1:k])) / H[i, i]
         comb = sum(y[i] * V[i] for i in range(k))

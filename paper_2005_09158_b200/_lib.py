@@ -151,6 +151,19 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def _hptr(t, numel: int, name: str):
+    """HOST buffer of the *_host entry points: a contiguous CPU float64 tensor of exactly `numel` elements (the C side
+    copies that many doubles in or out and cannot check host extents).  None passes through (optional inputs)."""
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous CPU float64 tensor (pinned recommended)")
+    if t.numel() != numel:
+        raise ValueError(f"{name}: expected {numel} elements, got {t.numel()}")
+    return C.c_void_p(t.data_ptr())
+
+
 class ParaDiag:
     """One ParaDiag-II context (pd_ctx) on the current CUDA device and stream.
 
@@ -311,24 +324,28 @@ class ParaDiag:
 
     def apply_precond_host(self, r_host, z_host):
         """r_host, z_host: contiguous CPU float64 tensors (pinned recommended) of shape [Nt, S]."""
+        n = self.nt * self.S
         _check(self._lib, self._ctx, self._lib.pd_apply_precond_host(
-            self._ctx, C.c_void_p(r_host.data_ptr()), C.c_void_p(z_host.data_ptr())))
+            self._ctx, _hptr(r_host, n, "r_host"), _hptr(z_host, n, "z_host")))
         return z_host
 
     def solve_ivp_host(self, solver: int, u0_host, u_host, v0_host=None, f_host=None, tol=1e-10, m=20, maxit=100):
         """End to end from HOST initial data (pinned CPU float64 tensors); u_host [Nt, S] receives the solution.
         solver: 0 stationary, 1 GMRES, 2 / 3 their tail forms, 4 simplified Newton."""
         rep, hist = self._report(maxit + 2)
-        p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
-        st = self._lib.pd_solve_ivp_host(self._ctx, solver, p(u0_host), p(v0_host), p(f_host), p(u_host), tol, m,
-                                         maxit, C.byref(rep))
+        S = self.S
+        st = self._lib.pd_solve_ivp_host(self._ctx, solver, _hptr(u0_host, S, "u0_host"), _hptr(v0_host, S, "v0_host"),
+                                         _hptr(f_host, (self.nt + 1) * S, "f_host"),
+                                         _hptr(u_host, self.nt * S, "u_host"), tol, m, maxit, C.byref(rep))
         _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
         return u_host, self._mk(st, rep, hist)
 
     def solve_host(self, solver: int, b_host, u_host, tol, m=20, maxit=100):
+        """solver: 0 stationary, 1 GMRES, optionally | SOLVE_ZERO_GUESS; b_host, u_host [Nt, S] CPU float64."""
         rep, hist = self._report(maxit + 2)
-        st = self._lib.pd_solve_host(self._ctx, solver, C.c_void_p(b_host.data_ptr()),
-                                     C.c_void_p(u_host.data_ptr()), tol, m, maxit, C.byref(rep))
+        n = self.nt * self.S
+        st = self._lib.pd_solve_host(self._ctx, solver, _hptr(b_host, n, "b_host"), _hptr(u_host, n, "u_host"), tol, m,
+                                     maxit, C.byref(rep))
         _check(self._lib, self._ctx, st, allow=(PD_OK, PD_NOT_CONVERGED))
         return u_host, self._mk(st, rep, hist)
 

@@ -52,6 +52,12 @@ static void closed_form_spectra(int nt, double alpha, double dt, pd_scheme s, st
   l2.resize(nt);
   const long double pi = 3.141592653589793238462643383279502884L;
   const long double a = powl((long double)alpha, 1.0L / nt);
+  if (nt == 1) {  // reading t2: the 1 x 1 alpha-circulant is its first-column entry (no wrap, S:l.89)
+    const long double d = dt;
+    l1[0] = s == PD_LEAPFROG ? 1.0L / (d * d) : 1.0L / d;
+    l2[0] = s == PD_BE ? 1.0L : 0.5L;
+    return;
+  }
   for (int n = 0; n < nt; ++n) {
     // exact argument reduction of n/Nt before the trig call
     const long double th = 2.0L * pi * (long double)n / (long double)nt;
@@ -219,7 +225,7 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   if (!g) return fail(nullptr, PD_EINVAL, "grid is NULL");
   if (!(alpha > 0.0 && alpha <= 1.0)) return fail(nullptr, PD_EINVAL, "alpha=%g outside (0,1]", alpha);
   if (!(dt > 0.0)) return fail(nullptr, PD_EINVAL, "dt=%g must be > 0", dt);
-  if (!pd_tfft_supported(nt)) return fail(nullptr, PD_EINVAL, "Nt=%d must be a power of two in [2, 8192]", nt);
+  if (!pd_tfft_supported(nt)) return fail(nullptr, PD_EINVAL, "Nt=%d must be a power of two in [1, 8192]", nt);
   if (s != PD_BE && s != PD_CN && s != PD_LEAPFROG) return fail(nullptr, PD_EINVAL, "unknown scheme %d", (int)s);
   if (s == PD_LEAPFROG && nt < 4) return fail(nullptr, PD_EINVAL, "leapfrog needs Nt >= 4");
   if (!(g->length > 0.0)) return fail(nullptr, PD_EINVAL, "length must be > 0");
@@ -1139,12 +1145,14 @@ pd_status pd_apply_precond_host(pd_ctx* c, const double* rh, double* zh) {
 pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, double tol, int m, int maxit,
                         pd_report* rep) {
   if (!c || !bh || !uh) return c ? fail(c, PD_EINVAL, "null vector") : PD_EINVAL;
+  const bool zero = (solver & PD_SOLVE_ZERO_GUESS) != 0;
+  solver &= ~PD_SOLVE_ZERO_GUESS;
+  if (solver != 0 && solver != 1)
+    return fail(c, PD_EINVAL, "pd_solve_host: solver %d not in {0 stationary, 1 gmres} (| PD_SOLVE_ZERO_GUESS)", solver);
   pd_status s = ensure_stage(c);
   if (s != PD_OK) return s;
   const size_t bytes = sizeof(double) * c->nt * c->S;
   PD_CUDA(c, cudaMemcpyAsync(c->stage_a, bh, bytes, cudaMemcpyHostToDevice, c->st));
-  const bool zero = (solver & PD_SOLVE_ZERO_GUESS) != 0;
-  solver &= ~PD_SOLVE_ZERO_GUESS;
   if (!zero)
     PD_CUDA(c, cudaMemcpyAsync(c->stage_b, uh, bytes, cudaMemcpyHostToDevice, c->st));
   else if (solver == 0)

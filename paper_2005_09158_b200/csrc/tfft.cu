@@ -8,6 +8,8 @@
 // for all Nt time levels; two real columns are packed into one complex sequence (x + i y), transformed
 // with one complex FFT and separated again, so the tile is C complex FFTs of length Nt held in shared
 // memory (Nt*C*16 B, <= 128 KB).  HBM traffic per apply pass = 8 B/dof read + ~8 B/dof written.
+#include <algorithm>
+
 #include "fft.cuh"
 #include "kernels.h"
 
@@ -211,12 +213,28 @@ cudaError_t launch_inv_n(const double2* Sh, double* z, long long S, const double
   return cudaGetLastError();
 }
 
+// Nt = 1 (S:l.89; reading t2): a 1 x 1 alpha-circulant has no wrap entry, Gamma = [1] and the DFT of length 1 is
+// the identity, so Steps (a) / (c) only move the real column into / out of the complex spectrum buffer.
+__global__ void tfft1_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long long S) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < S; i += (long long)gridDim.x * blockDim.x)
+    Sh[i] = make_double2(r[i], 0.0);
+}
+__global__ void tfft1_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long long S, int acc) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < S; i += (long long)gridDim.x * blockDim.x)
+    z[i] = acc ? z[i] + Sh[i].x : Sh[i].x;
+}
+unsigned blocks1(long long S) { return (unsigned)std::min<long long>((S + 255) / 256, 148 * 8); }
+
 }  // namespace
 
-int pd_tfft_supported(int nt) { return nt >= 2 && nt <= 8192 && (nt & (nt - 1)) == 0; }
+int pd_tfft_supported(int nt) { return nt >= 1 && nt <= 8192 && (nt & (nt - 1)) == 0; }
 
 cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
                                const double2* tw, cudaStream_t st) {
+  if (nt == 1) {
+    tfft1_fwd_kernel<<<blocks1(S), 256, 0, st>>>(r, Sh, S);
+    return cudaGetLastError();
+  }
   switch (nt) {
 #define PD_CASE(n) \
   case n:          \
@@ -231,6 +249,10 @@ cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S
 
 cudaError_t pd_launch_tfft_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
                                const double2* tw, int accumulate, cudaStream_t st) {
+  if (nt == 1) {
+    tfft1_inv_kernel<<<blocks1(S), 256, 0, st>>>(Sh, z, S, accumulate);
+    return cudaGetLastError();
+  }
   switch (nt) {
 #define PD_CASE(n) \
   case n:          \

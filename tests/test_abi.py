@@ -48,3 +48,20 @@ def test_setup_rejects_invalid_arguments(lib, kw, needle):
 def test_null_pointers_rejected(lib):
     assert lib.pd_apply_precond(None, None, None) == -1
     assert lib.pd_local_size(None) == -1
+
+
+def test_host_buffer_checks():
+    """The *_host entry points copy Nt * S doubles from / to host memory the library cannot bound-check: the binding
+    refuses anything but a contiguous CPU float64 tensor of exactly that many elements."""
+    import torch
+    ok = torch.zeros(4, 8, dtype=torch.float64)
+    assert _lib._hptr(ok, 32, "x").value == ok.data_ptr()
+    assert _lib._hptr(None, 32, "x") is None
+    with pytest.raises(TypeError):
+        _lib._hptr(ok.float(), 32, "x")                 # float32
+    with pytest.raises(TypeError):
+        _lib._hptr(ok.t(), 32, "x")                     # non-contiguous view
+    with pytest.raises(ValueError):
+        _lib._hptr(ok[:3], 32, "x")                     # f with Nt rows instead of Nt + 1, etc.
+    with pytest.raises(TypeError):
+        _lib._hptr(ok.numpy(), 32, "x")                 # not a tensor

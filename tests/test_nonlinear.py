@@ -77,5 +77,20 @@ def test_nl_gpu_matches_oracle(scheme, nx, nt):
     u_ref, rep_ref = NL.solve_newton(cfg, RX, b)
     assert rep.converged and rep.iterations == rep_ref.iterations, (rep.history, rep_ref.history)
     assert rel(to_host(u), u_ref) < 1e-8
+    floor = residual_floor(cfg, b, u_ref)
+    print(f"newton {nx}x{nt}: residual rounding floor {floor:.2e}")
     for a, c in zip(rep.history, rep_ref.history):
-        assert abs(a - c) <= 1e-6 * c + 1e-12  # relative residuals: rounding floor ~1e-13
+        assert abs(a - c) <= 1e-6 * c + floor
+
+
+def residual_floor(cfg, b, u):
+    """Rounding floor of a relative residual ||b - (B1 u + B2 F(u))|| / ||b|| computed in fp64 (DESIGN.md reading
+    n1): each entry is a sum of O(10) products, so its absolute error is of order eps times the same sum taken over
+    absolute values, |b| + |B1| |u| + |B2| (|K| |u| + |g(u)|) (8 eps used); the history entries near tol are
+    differences of such sums and cannot agree below it (1023 x 1024: 1.8e-12; 4095 x 16, where |K| = 3.4e5: 2e-10)."""
+    c1, c2 = problems.time_first_columns(cfg)
+    absK = abs(problems.K_matrix(cfg))
+    au = np.abs(u)
+    kg = np.ascontiguousarray((absK @ au.T).T) + np.abs(RX.g(u))
+    tot = np.abs(b) + problems.apply_time(np.abs(c1), au, None) + problems.apply_time(np.abs(c2), kg, None)
+    return 8 * np.finfo(np.float64).eps * float(np.linalg.norm(tot) / np.linalg.norm(b))

@@ -196,6 +196,28 @@ def test_apply_O1_equals_O2_medium(name):
     assert rel(problems.matvec_P(cfg, z1), r) < 1e-10
 
 
+@pytest.mark.slow
+def test_wave_rounding_floor_reading_t1():
+    """Reading t1: on the config-2 recipe (leapfrog, alpha = 1e-2, T = 2, resonant systems) the two
+    fp64 oracles' forward errors against an extended-precision reference (O2 modal in np.longdouble, whose backward
+    error ||P_alpha z - r|| / ||r|| in longdouble is 6e-16) are of the size of their mutual distance delta and grow
+    with the size, O1 (dense DFT-matrix sums) the most: the fp64 floor, amplified by Cond_2(V) <= 1/alpha (eq 2.13),
+    not a defect of either oracle.  Measured: 1023 x 1024 delta 2.0e-11, O1 2.0e-11, O2 4.1e-12; 2047 x 2048 delta
+    8.7e-11, O1 1.0e-10, O2 3.0e-11; full config 2 delta 4.8e-10."""
+    cfg = W.CONFIGS[2].scaled(nx=1023, nt=1024)
+    r = W.random_vector(cfg, seed=7)
+    z1 = spectral.apply_precond(cfg, r)
+    z2 = periodic.apply_precond_modal(cfg, r)
+    zl = periodic.apply_precond_modal(cfg, r, precision=np.longdouble)
+    c1, c2 = problems.time_first_columns(cfg)
+    pz = problems.apply_time(c1, zl, cfg.alpha) + problems.apply_K(cfg, problems.apply_time(c2, zl, cfg.alpha))
+    assert float(np.linalg.norm(pz - r) / np.linalg.norm(r)) < 1e-14    # measured 6.4e-16 (|K| ~ 4/h^2 = 4e6)
+    delta = rel(z1, z2)
+    e1, e2 = float(rel(z1, zl)), float(rel(z2, zl))
+    assert 1e-12 < delta < 1e-10
+    assert e2 < e1 <= 2 * delta and delta <= e1 + e2
+
+
 def test_apply_special_cases():
     cfg = tiny(W.ADE1D, W.BE, nx=9, nt=1)
     r = np.random.default_rng(3).standard_normal((1, 9))
@@ -330,6 +352,26 @@ def test_converged_solution_equals_sequential(name, solver, expect):
         for i in range(1, len(h)):
             if h[i - 1] > 1e-13:
                 assert h[i] / h[i - 1] <= 1.5 * cfg.alpha / (1 - cfg.alpha) + 1e-3
+
+
+@pytest.mark.parametrize("cfg", [W.CONFIGS[4].scaled(nx=32, ny=32, nt=64), W.CONFIGS[3].scaled(nx=16, ny=16, nt=32),
+                                 W.ctp01_config(W.CN, 1e-2, nx=32, ny=32, nt=16)], ids=["cfg4s", "cfg3s", "ctp01s"])
+def test_march_fourier_equals_sparse_march(cfg):
+    """stepping.march_fourier (eq 2.4 per 2D Fourier mode, used at config-4 size) = stepping.march (sparse LU per
+    step), with and without a source; and a single mode e_k decays by the scalar amplification factor."""
+    u0 = W.initial_u0(cfg)
+    f = np.random.default_rng(1).standard_normal((cfg.nt + 1, cfg.S))
+    assert rel(stepping.march_fourier(cfg, u0), stepping.march(cfg, u0)) < 1e-13
+    assert rel(stepping.march_fourier(cfg, u0, f), stepping.march(cfg, u0, None, f)) < 1e-13
+    X, Y = W.grid(cfg)
+    n, kx, ky = cfg.nx, 3, 1
+    th = problems.theta_of(cfg.scheme)
+    kap = spectral.symbol_2d(cfg)[ky, kx]
+    g = (1 / cfg.dt - (1 - th) * kap) / (1 / cfg.dt + th * kap)
+    mode = np.exp(2j * math.pi / cfg.length * (kx * X + ky * Y)).reshape(-1)
+    u = stepping.march_fourier(cfg, mode.real)  # Re e_k = (e_k + e_-k)/2, kappa(-k) = conj kappa(k)
+    ex = np.real(g ** np.arange(1, cfg.nt + 1)[:, None] * mode[None, :])
+    assert rel(u, ex) < 1e-12
 
 
 def test_residual_definitions():

@@ -79,6 +79,46 @@ def test_t4a_golden_matches_table_claims():
         assert p / 2 <= e <= p                                # reading x4: a constant factor ~1.6 below print
 
 
+COUNTS = os.path.join(os.path.dirname(__file__), "golden", "t4a_alpha1_counts.json")
+
+
+def _alpha1_counts():
+    with open(COUNTS) as fh:
+        return json.load(fh)
+
+
+def test_t4a_alpha1_count_not_fixed_in_fp64():
+    """Reading x4: at alpha = 1 the GMRES count is not determined by the method in fp64.  Three correct references
+    (tools/t4a_alpha1_counts.py, oracle only) -- O1 (time DFT + sparse LU), O2 (alpha-periodic stepping in the DST
+    basis) and O2 with the whole GMRES in x87 extended precision -- agree on the first two Arnoldi residuals, then
+    stagnate in pairs a few times above tol (the Arnoldi residual of a plateau pair is nearly constant) and cross
+    tol at different iterations: L = 64 gives 9 / 7 / 7, L = 128 gives 13 / 9 / 7 (the paper prints 7 and 37).
+    The GPU count is therefore pinned to the range of these references, per mesh (test_t4a_gpu_matches_oracle)."""
+    g = _alpha1_counts()
+    names = ("O1_fp64", "O2_fp64", "O2_longdouble")
+    for L in (32, 64, 128):
+        runs = [g["runs"][f"{L}_{n}"] for n in names]
+        assert all(r["converged"] and r["rel_residual"] <= 1e-10 for r in runs)
+        h0 = runs[0]["history"]
+        for r in runs[1:]:
+            for a, c in zip(r["history"][:2], h0[:2]):        # before the plateau: the same Krylov residuals
+                assert abs(a - c) <= 1e-6 * c
+        for r in runs:
+            h = r["history"]
+            assert 1e-10 < h[2] < 1e-7 and h[3] >= 0.97 * h[2]  # iteration 3 lands on a plateau pair above tol
+        counts = [r["iterations"] for r in runs]
+        if L == 32:
+            assert counts == [5, 5, 5]
+        else:
+            assert max(counts) - min(counts) >= 2, counts     # three correct references, three different counts
+    # the golden is the oracle's: O1 and O2 in fp64 re-run live at L = 64 (~15 s) disagree by two iterations
+    cfg = W.t4a_config(64, 1.0)
+    b = problems.rhs(cfg, W.initial_u0(cfg), W.initial_v0(cfg), W.source_samples(cfg))
+    _, r1 = solvers.solve_gmres(cfg, b, tol=1e-10, m=50, maxit=50)
+    _, r2 = solvers.solve_gmres(cfg, b, tol=1e-10, m=50, maxit=50, apply=lambda r: periodic.apply_precond_modal(cfg, r))
+    assert (r1.iterations, r2.iterations) == (g["runs"]["64_O1_fp64"]["iterations"], g["runs"]["64_O2_fp64"]["iterations"])
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("label,alpha", [(32, 0.1), (64, 0.1), (128, 0.1), (256, 0.1), (32, 1.0), (64, 1.0),
                                          (128, 1.0)])
@@ -93,9 +133,10 @@ def test_t4a_gpu_matches_oracle(label, alpha):
     if alpha < 1.0:
         assert rep.iterations == run["iterations"]
     else:
-        # alpha = 1: the residual plateaus in pairs at ~tol (golden histories: 3.33e-10, 3.32e-10, 8.6e-11 at
-        # L = 64), so the last count is decided by rounding in the near-singular shifted systems (reading x4)
-        assert abs(rep.iterations - run["iterations"]) <= 2
+        # alpha = 1: not fixed in fp64 (test_t4a_alpha1_count_not_fixed_in_fp64): within the references' range
+        refs = [_alpha1_counts()["runs"][f"{label}_{n}"]["iterations"] for n in ("O1_fp64", "O2_fp64", "O2_longdouble")]
+        print(f"T4A L={label} alpha=1: GPU {rep.iterations} its, references O1/O2/O2-longdouble {refs}")
+        assert min(refs) <= rep.iterations <= max(refs), (rep.iterations, refs)
     ex = W.exact_wave_solution(cfg)
     uh = to_host(u)
     err = np.sqrt(cfg.h ** 2 * np.sum((uh - ex) ** 2, axis=1)).max()
