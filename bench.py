@@ -26,7 +26,14 @@ import workloads as W  # noqa: E402
 
 METRIC = "P_alpha^{-1} applies/s and solve time (Nt*Nx dofs/s, % HBM roofline) at 1/2/4/8 GPU"
 FALLBACK_HBM = 6650.0
-PHASES = ["tfft_fwd", "spatial_solve", "tfft_inv", "residual", "tfft_inv_update", "matvec", "krylov_blas1"]
+PHASES = ["tfft_fwd", "spatial_solve", "tfft_inv", "residual", "tfft_inv_update", "matvec", "krylov_blas1",
+          "residual_norm"]
+T_START = time.perf_counter()
+
+
+def log(msg):
+    """Bench stage timestamps on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench {time.perf_counter() - T_START:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def hbm_peak():
@@ -39,10 +46,14 @@ def hbm_peak():
 
 
 def phase_bytes(cfg, S_local):
-    """Algorithmic HBM bytes per launch of each timed kernel."""
+    """Algorithmic HBM bytes per launch of each timed slot: the time FFTs read or write
+    8 B/dof real and the half spectrum (Nt/2+1) S 16 B; Step (b) reads and writes the half spectrum; the residual
+    b - A u reads u, b and writes r (24 B/dof), its norm-only form (slot 7, GMRES cycle ends) reads u, b (16 B/dof);
+    the matvec reads u and writes A u (16 B/dof).  Slot 6 (Krylov sweeps) has no fixed count."""
     D = cfg.nt * S_local
     spec = (cfg.nt // 2 + 1) * S_local * 16
-    return {0: D * 8 + spec, 1: 2 * spec, 2: spec + D * 8, 3: 3 * D * 8, 4: spec + 2 * D * 8, 5: 2 * D * 8}
+    return {0: D * 8 + spec, 1: 2 * spec, 2: spec + D * 8, 3: 3 * D * 8, 4: spec + 2 * D * 8, 5: 2 * D * 8,
+            7: 2 * D * 8}
 
 
 def oracle_sample_cfg(cfg):
@@ -72,12 +83,63 @@ def blas_threads():
         return os.cpu_count()
 
 
-def cpu_baseline(cfg):
+def host_cpu():
+    """nproc and the lscpu model line of the host the CPU legs ran on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def cpu_baseline(cfg, full=False):
+    """The oracle (kind "oracle", the contract's key) plus BASELINE.md §3's fair CPU comparisons: the fast CPU
+    ParaDiag-II (tools/cpu_fast.py: scipy.fft with workers = nproc, Thomas vectorised over frequencies) on the same
+    sample and on the whole workload when it fits the host's memory, and sequential time stepping (the classical
+    route, P:l.76-78) on the whole workload."""
     s = oracle_sample_cfg(cfg)
+    log(f"cpu: oracle O1 solve on {s.nx}x{s.ny}x{s.nt}")
     sec, rep = run_oracle_solve(s)
-    return {"value": s.D / sec, "unit": "dofs/s", "cores": blas_threads(), "kind": "oracle",
-            "sample": f"{cfg.name} recipe at Nx={s.nx}x{s.ny}, Nt={s.nt} ({s.D} dofs): one oracle O1 "
-                      f"{s.solver} solve ({rep.iterations} its) in {sec:.2f} s on the host cores"}
+    out = {"value": s.D / sec, "unit": "dofs/s", "cores": blas_threads(), "kind": "oracle",
+           "sample": f"{cfg.name} recipe at Nx={s.nx}x{s.ny}, Nt={s.nt} ({s.D} dofs): one oracle O1 "
+                     f"{s.solver} solve ({rep.iterations} its) in {sec:.2f} s on the host cores",
+           "host": host_cpu()}
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import cpu_fast
+    log("cpu: fast CPU reference on the oracle's sample")
+    t_pd, its, t_seq, err = cpu_fast.timed_solve(s)
+    out["fast_cpu_sample"] = {"value": s.D / t_pd, "unit": "dofs/s", "iterations": its, "seconds": round(t_pd, 3),
+                              "cores": cpu_fast.NPROC, "kind": "fast CPU ParaDiag-II (tools/cpu_fast.py)",
+                              "sample": f"Nx={s.nx}x{s.ny}, Nt={s.nt}"}
+    out["sequential_sample"] = {"value": s.D / t_seq, "unit": "dofs/s", "seconds": round(t_seq, 3),
+                                "kind": "sequential time stepping (tools/cpu_fast.py)", "rel_diff_vs_paradiag": err}
+    if cfg.D > s.D:
+        # the whole workload when the host holds it: sequential stepping (one [Nt][S] array) always, the fast
+        # ParaDiag-II (GMRES(m): m + 1 vectors plus ~7 work arrays) with --cpu-full (minutes on cfg4)
+        try:
+            avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        except (ValueError, OSError):
+            avail = 0
+        if full and (cfg.m + 8) * cfg.D * 8 < 0.6 * avail:
+            log("cpu: fast CPU reference on the whole workload")
+            t_pd, its, t_seq, err = cpu_fast.timed_solve(cfg)
+            out["fast_cpu_full"] = {"value": cfg.D / t_pd, "unit": "dofs/s", "iterations": its,
+                                    "seconds": round(t_pd, 3), "cores": cpu_fast.NPROC,
+                                    "kind": "fast CPU ParaDiag-II, whole workload"}
+            out["sequential_full"] = {"value": cfg.D / t_seq, "unit": "dofs/s", "seconds": round(t_seq, 3),
+                                      "kind": "sequential time stepping, whole workload", "rel_diff_vs_paradiag": err}
+        elif 3 * cfg.D * 8 < 0.6 * avail:
+            log("cpu: sequential stepping on the whole workload")
+            t0 = time.perf_counter()
+            cpu_fast.sequential(cfg, W.initial_u0(cfg), W.initial_v0(cfg), W.source_samples(cfg))
+            t_seq = time.perf_counter() - t0
+            out["sequential_full"] = {"value": cfg.D / t_seq, "unit": "dofs/s", "seconds": round(t_seq, 3),
+                                      "kind": "sequential time stepping, whole workload (tools/cpu_fast.py)"}
+    return out
 
 
 class ClockSampler:
@@ -166,10 +228,23 @@ def main():
     ap.add_argument("--apply-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="also run the fast CPU ParaDiag-II on the whole workload")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torchrun (the driver's own multi-GPU launch sets WORLD_SIZE itself)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execve(sys.executable, cmd, env)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     cfg = W.BY_NAME[args.config]
 
     if args.impl == "reference":
@@ -188,6 +263,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
+    log(f"setup {cfg.name} on {world} rank(s)")
     ctx = ParaDiag(**ctor_args(cfg), stream=stream, rank=rank, size=world, nccl_id=nccl_id)
 
     def barrier():
@@ -212,9 +288,11 @@ def main():
             return ctx.solve_stationary(b, u, tol=cfg.tol, maxit=cfg.maxit)[1]
         return ctx.solve_gmres(b, u, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit, zero_guess=True)[1]
 
+    log("warm-up")
     for _ in range(args.warmup):
         rep = step()
     barrier()
+    log("timed steps")
     launches0 = ctx.kernel_launches()
     ctx.enable_phase_timing(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -240,6 +318,7 @@ def main():
     value = cfg.D / (ms / 1e3)
 
     # ---- the same solve in WR tail form (single GPU): same iterates, reported beside ----
+    log("tail form")
     tail_form = None
     if world == 1:
         def step_tail():
@@ -266,6 +345,7 @@ def main():
                              "last H time blocks are carried (tail map + O(H S) vector work)"}
 
     # ---- apply throughput (same stream, inputs > L2) ----
+    log("apply throughput")
     r = torch.randn(ctx.shape, dtype=torch.float64, device="cuda")
     z = torch.empty_like(r)
     for _ in range(3):
@@ -287,7 +367,7 @@ def main():
 
     # ---- dominant kernel roofline ----
     pb = phase_bytes(cfg, ctx.S)
-    dom = max(range(6), key=lambda i: pms[i])  # dominant kernel with a fixed algorithmic byte count
+    dom = max(pb, key=lambda i: pms[i])  # dominant kernel (largest share) among those with a fixed byte count
     dom_ms = pms[dom] / max(pn[dom], 1)
     achieved = pb[dom] / (dom_ms / 1e3) / 1e9
     traffic = None
@@ -301,8 +381,9 @@ def main():
     phases = {PHASES[i]: {"ms_per_call": round(pms[i] / pn[i], 4), "calls": int(pn[i]),
                           "share_of_step": round(pms[i] / (ms * args.steps), 4),
                           "GBps": round(pb[i] / (pms[i] / pn[i] / 1e3) / 1e9, 1) if i in pb else None}
-              for i in range(7) if pn[i]}
+              for i in range(8) if pn[i]}
 
+    log("end to end")
     # ---- end to end through the host C ABI (pd_solve_ivp_host): H2D of the step's inputs (the initial data and
     # source samples) from pinned host memory, b built on the device, the solve, D2H of the space-time solution ----
     e2e = None
@@ -343,7 +424,11 @@ def main():
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
+        del ctx, b, u
+        torch.cuda.empty_cache()
+        all_host_threads()
+        cpu = cpu_baseline(cfg, full=args.cpu_full)
+        log("cpu legs done")
     out = {
         "metric": METRIC, "value": value, "unit": "dofs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -373,10 +458,20 @@ def main():
         dist.destroy_process_group()
 
 
+def all_host_threads():
+    """torchrun sets OMP_NUM_THREADS=1 for every rank; the CPU legs run on rank 0 alone and use all host cores."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        pass
+
+
 def run_reference(args, cfg, rank, world):
     """The oracle arm: the CPU oracle as it stands, on bounded samples of the same workload."""
     if rank != 0:
         return
+    all_host_threads()
     s = oracle_sample_cfg(cfg)
     for _ in range(args.warmup):
         run_oracle_solve(s)
