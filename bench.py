@@ -256,15 +256,17 @@ def main():
     from tests.helpers import ctor_args
 
     torch.cuda.set_device(local)
-    nccl_id = None
+    nccl_id = comm_ptr = None
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        comm_ptr = pg_nccl_comm()
+        if comm_ptr is None:  # no handle on the process group's communicator: a second one from a unique id
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
     stream = torch.cuda.current_stream()
-    log(f"setup {cfg.name} on {world} rank(s)")
-    ctx = ParaDiag(**ctor_args(cfg), stream=stream, rank=rank, size=world, nccl_id=nccl_id)
+    log(f"setup {cfg.name} on {world} rank(s) (communicator: {'process group' if comm_ptr else 'unique id'})")
+    ctx = ParaDiag(**ctor_args(cfg), stream=stream, rank=rank, size=world, nccl_id=nccl_id, nccl_comm=comm_ptr)
 
     def barrier():
         torch.cuda.synchronize()
@@ -456,6 +458,18 @@ def main():
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def pg_nccl_comm():
+    """ncclComm_t of the default (eagerly connected) ProcessGroupNCCL, or None when torch does not expose it."""
+    import torch
+    import torch.distributed as dist
+    try:
+        be = dist.group.WORLD._get_backend(torch.device("cuda"))
+        ptr = int(be._comm_ptr())
+        return ptr or None
+    except Exception:
+        return None
 
 
 def all_host_threads():

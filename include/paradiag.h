@@ -71,13 +71,17 @@ typedef struct {
  * x-range, 2D: a range of y-rows); Step (b) runs on frequency shards after an all-to-all over NCCL.
  *   size == 1              single GPU (rank must be 0, nccl_id ignored)
  *   size > 1, rank >= 0    NCCL rank `rank` of `size`; vectors passed to the context are the LOCAL slab
- *                          [Nt][S_local] (pd_local_shape); nccl_id from pd_nccl_unique_id on one rank
+ *                          [Nt][S_local] (pd_local_shape).  Communicator: nccl_comm when non-NULL (an existing
+ *                          ncclComm_t of exactly these ranks, e.g. torch's ProcessGroupNCCL._comm_ptr(); borrowed,
+ *                          never destroyed by the library), else a new one from nccl_id (pd_nccl_unique_id on one
+ *                          rank, shared by all; owned and destroyed by pd_destroy)
  *   size > 1, rank < 0     `size` virtual ranks inside this process on one GPU: vectors are GLOBAL, every
  *                          exchange of the plan is executed with device copies (test mode of the sharded
  *                          path; same plan, partition and kernels as the NCCL mode) */
 typedef struct {
   int rank, size;
-  const void* nccl_id;          /* 128-byte ncclUniqueId shared by all ranks */
+  const void* nccl_id;          /* 128-byte ncclUniqueId shared by all ranks (used when nccl_comm is NULL) */
+  void* nccl_comm;              /* borrowed ncclComm_t of the caller's process group, or NULL */
 } pd_dist;
 
 typedef struct {
@@ -208,7 +212,9 @@ PD_API long long pd_kernel_launches(const pd_ctx* ctx);
  * kernel of the path, without host synchronisation, and pd_phase_times (which synchronises) returns the
  * accumulated device milliseconds and launch counts per slot:
  *   0 Step (a) time FFT, 1 Step (b) spatial solve, 2 Step (c) inverse time FFT, 3 residual b - A u,
- *   4 Step (c) fused with the update u += z, 5 matvec A u, 6-7 reserved.   ms8, count8: HOST arrays of 8. */
+ *   4 Step (c) fused with the update u += z, 5 matvec A u, 6 Krylov sweeps (and the GMRES final update whose
+ *   combination the forward time FFT reads), 7 norm-only residual ||b - A u|| (no vector written; GMRES cycle ends).
+ *   ms8, count8: HOST arrays of 8. */
 PD_API pd_status pd_enable_phase_timing(pd_ctx* ctx, int enable);
 PD_API pd_status pd_phase_times(pd_ctx* ctx, double* ms8, long long* count8);
 

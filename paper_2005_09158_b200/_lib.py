@@ -30,7 +30,7 @@ class pd_grid(C.Structure):
 
 
 class pd_dist(C.Structure):
-    _fields_ = [("rank", C.c_int), ("size", C.c_int), ("nccl_id", C.c_void_p)]
+    _fields_ = [("rank", C.c_int), ("size", C.c_int), ("nccl_id", C.c_void_p), ("nccl_comm", C.c_void_p)]
 
 
 class pd_report(C.Structure):
@@ -174,7 +174,7 @@ class ParaDiag:
 
     def __init__(self, op: int, nx: int, ny: int, length: float, nu: float, ax: float, ay: float,
                  dt: float, nt: int, alpha: float, scheme: int, stream=None, rank: int = 0, size: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, nccl_comm: int | None = None):
         import torch
         self._lib = load_library()
         if not torch.cuda.is_available():
@@ -182,7 +182,8 @@ class ParaDiag:
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         g = pd_grid(op, nx, ny, length, nu, ax, ay)
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        d = pd_dist(rank, size, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
+        d = pd_dist(rank, size, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None,
+                    C.c_void_p(nccl_comm) if nccl_comm else None)
         self.rank, self.size = rank, size
         self.scheme = scheme
         ctx = C.c_void_p()

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparadiag.so")
-SOURCES = ["paradiag.cpp", "dist.cpp", "comm.cpp", "tfft.cu", "tfft4.cu", "tfx.cu", "tridiag.cu", "slab2d.cu", "stencil.cu", "blas1.cu", "tail.cu", "tailform.cpp", "nonlin.cu", "newton.cpp"]
+SOURCES = ["paradiag.cpp", "dist.cpp", "comm.cpp", "tfft.cu", "tfft4.cu", "tfx.cu", "tridiag.cu", "slab2d.cu", "stencil.cu", "blas1.cu", "tail.cu", "tailform.cpp", "nonlin.cu", "newton.cpp", "gtsv.cu", "tf4_tma.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]

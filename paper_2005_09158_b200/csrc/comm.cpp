@@ -76,6 +76,7 @@ struct pd_comm {
   ncclComm_t comm = nullptr;
   int rank = 0, size = 1;
   cudaStream_t st = nullptr;
+  bool owned = true;
 };
 
 const char* pd_comm_last_error() { return g_err.c_str(); }
@@ -103,9 +104,20 @@ pd_comm* pd_comm_create(const void* id, int rank, int size, cudaStream_t st) {
   return c;
 }
 
+pd_comm* pd_comm_wrap(void* nccl_comm, int rank, int size, cudaStream_t st) {
+  if (!load()) return nullptr;
+  pd_comm* c = new pd_comm();
+  c->comm = static_cast<ncclComm_t>(nccl_comm);
+  c->rank = rank;
+  c->size = size;
+  c->st = st;
+  c->owned = false;
+  return c;
+}
+
 void pd_comm_destroy(pd_comm* c) {
   if (!c) return;
-  if (c->comm && g_api.commDestroy) g_api.commDestroy(c->comm);
+  if (c->owned && c->comm && g_api.commDestroy) g_api.commDestroy(c->comm);
   delete c;
 }
 

@@ -9,6 +9,8 @@ struct pd_comm;
 
 int pd_comm_unique_id(void* out128);
 pd_comm* pd_comm_create(const void* id, int rank, int size, cudaStream_t st);
+// borrow an existing ncclComm_t (e.g. the caller's torch ProcessGroupNCCL communicator): not destroyed
+pd_comm* pd_comm_wrap(void* nccl_comm, int rank, int size, cudaStream_t st);
 void pd_comm_destroy(pd_comm* c);
 const char* pd_comm_last_error();
 int pd_comm_group_start(pd_comm* c);

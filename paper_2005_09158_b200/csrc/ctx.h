@@ -82,7 +82,10 @@ struct pd_ctx {
   double2* tw_s = nullptr;       // 2D: exp(-2 pi i j / N)
   pd_ytri_coef* ytri = nullptr;  // 2D: [F][N] cyclic Toeplitz y-pass constants (slab2d.cu ytri)
   double* nl_dbar = nullptr;     // NEXT-4: time-averaged reaction Jacobian [S]
-  double2* nl_cp = nullptr;      // NEXT-4: Thomas c' scratch [F][S]
+  bool use_gtsv = false;         // 1D Step (b) by pivoted elimination (gtsv.cu) instead of the recurrences
+  void* gtsv_scratch = nullptr;  // gtsv factors [F][Nx] (1/d, du, swap flags), allocated on first use
+  int* gtsv_bad = nullptr;       // device: max (frequency + 1) with a zero / non-finite pivot (0: none)
+  int* gtsv_hbad = nullptr;      // pinned host copy
   double* mu = nullptr;          // 2D Dirichlet: [M] DST eigenvalues (4 nu/h^2) sin^2(pi k / M), M = 2(N+1)
   bool use_ytri = false;
   pd_slab_params slab{};
@@ -166,7 +169,7 @@ pd_status fail(pd_ctx* c, pd_status s, const char* fmt, ...);
   } while (0)
 
 // dist.cpp
-pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id);
+pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id, void* nccl_comm);
 void pd_dist_free(pd_ctx* c);
 pd_status pd_dist_apply(pd_ctx* c, const double* r, double* z, int accumulate);
 pd_status pd_dist_stencil(pd_ctx* c, const double* b, const double* u, double* out, double* norm2_dev_partial_sum);
@@ -181,5 +184,6 @@ extern "C" void pd_report_push(pd_report* rep, double v);
 void pd_tail_free(pd_ctx* c);
 void pd_corner_coefs(const pd_ctx* c, pd_tail_g* gc);
 pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0);
+pd_status pd_gtsv_ensure(pd_ctx* c);
 pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S);
 pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate);

@@ -66,7 +66,7 @@ extern "C" pd_status pd_partition(int op, int nx, int ny, int nt, int size, long
 
 static int hw_of(const pd_ctx* c) { return pd_is_2d(c->g.op) ? c->g.nx : 1; }
 
-pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id) {
+pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id, void* nccl_comm) {
   const int P = c->size;
   c->plan = pd_make_plan(c->g.op, c->g.nx, c->g.ny, c->nt, P);
   const pd_plan& pl = c->plan;
@@ -76,7 +76,7 @@ pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id) {
   const int hw = hw_of(c);
   std::vector<int> ranks;
   if (c->dist_mode == 1) {
-    c->comm = pd_comm_create(nccl_id, c->rank, P, c->st);
+    c->comm = nccl_comm ? pd_comm_wrap(nccl_comm, c->rank, P, c->st) : pd_comm_create(nccl_id, c->rank, P, c->st);
     if (!c->comm) return fail(c, PD_ENCCL, "NCCL init: %s", pd_comm_last_error());
     ranks.push_back(c->rank);
   } else {

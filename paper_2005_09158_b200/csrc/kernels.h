@@ -88,6 +88,11 @@ inline cudaError_t ov_join(const pd_tfx_overlap* ov, cudaStream_t st) {
   }
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
+// forward stage 1 through TMA (tf4_tma.cu; PD_TMA=1): same output as tf4_fwd_s1<NT, N2 = 256, ...>
+int pd_tf4_tma_supported(int nt, long long S, const void* r);
+cudaError_t pd_launch_tf4_fwd_s1_tma(int nt, const double* r, long long S, long long p_begin, long long pc,
+                                     double2* Y, const double* gam, const double2* tw2, const double2* twt,
+                                     cudaStream_t st);
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr,
@@ -196,8 +201,9 @@ cudaError_t pd_launch_any_nonzero(const double* x, long long n, int* flag, cudaS
 // ---- nonlinear ParaDiag-II, simplified Newton (nonlin.cu, oracle/nonlinear.py) ----
 // dbar[x] = (1/Nt) sum_n (3 g3 u_n(x)^2 + g1): the time-averaged reaction Jacobian (P:l.214-216)
 cudaError_t pd_launch_jac_avg(const double* u, double* dbar, int nt, long long S, double g3, double g1, cudaStream_t st);
-// Step (b) with J = K + diag(dbar): per frequency n the tridiagonal (lambda2 sub, lambda1 + lambda2 (dia + dbar_i),
-// lambda2 sup) by the Thomas algorithm (no pivoting: diagonally dominant at these shifts), one thread per
-// frequency; cp: [nfreq][nx] complex scratch
-cudaError_t pd_launch_thomas_shift(double2* Sh, int nx, int nfreq, const double2* lam1, const double2* lam2, double sub,
-                                   double dia, double sup, const double* dbar, double2* cp, cudaStream_t st);
+// Step (b), 1D, general: per frequency n the tridiagonal (lambda2 sub, lambda1 + lambda2 (dia + dbar_i), lambda2 sup)
+// (dbar nullable: 0) by Gaussian elimination with partial pivoting (gtsv.cu), one lane per frequency; scratch of
+// pd_gtsv_scratch_bytes; *bad = max (n + 1) over frequencies with a zero / non-finite pivot (caller zeroes it)
+size_t pd_gtsv_scratch_bytes(int nx, int nfreq);
+cudaError_t pd_launch_gtsv_shift(double2* Sh, int nx, int nfreq, const double2* lam1, const double2* lam2, double sub,
+                                 double dia, double sup, const double* dbar, void* scratch, int* bad, cudaStream_t st);

@@ -122,12 +122,42 @@ static bool ytri_coefs(const pd_ctx* c, const std::vector<cld>& l1, const std::v
   return true;
 }
 
-// per-frequency constants of the Toeplitz tridiagonal recurrence solver (tridiag.cu)
+// Host check of the pivoted elimination (gtsv.cu) on one constant-coefficient shifted system, in long double: the
+// smallest |pivot| relative to the largest matrix entry (0 = singular).  Used when the recurrence solver does not apply.
+static long double gtsv_min_pivot(cld A, cld B, cld Cc, int N) {
+  auto c1 = [](cld v) { return fabsl(v.real()) + fabsl(v.imag()); };
+  const long double scale = std::max(c1(A), std::max(c1(B), c1(Cc)));
+  cld cd = B, cdu = N > 1 ? Cc : 0.0L;
+  long double mn = INFINITY;
+  for (int j = 1; j < N; ++j) {
+    const cld ndu = j < N - 1 ? Cc : 0.0L;
+    if (c1(cd) >= c1(A)) {
+      mn = std::min(mn, c1(cd));
+      if (c1(cd) == 0) return 0;
+      const cld l = A / cd;
+      cd = B - l * cdu;
+      cdu = ndu;
+    } else {
+      mn = std::min(mn, c1(A));
+      const cld l = cd / A;
+      cd = cdu - l * B;
+      cdu = -l * ndu;
+    }
+  }
+  mn = std::min(mn, c1(cd));
+  return scale > 0 ? mn / scale : 0;
+}
+
+// per-frequency constants of the Toeplitz tridiagonal recurrence solver (tridiag.cu).  When a shifted system leaves
+// the recurrence's stable regime (or PD_TRIDIAG_GTSV=1), the context switches to the pivoted elimination (gtsv.cu)
+// for every frequency; singular shifts are then detected by the same elimination on the host (reading t4).
 static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vector<cld>& l2, double sub, double dia,
                            double sup, std::vector<pd_tri_coef>& out) {
   const int N = c->g.nx, L = pd_tridiag_rows_per_thread();
   out.resize(c->F);
-  for (int n = 0; n < c->F; ++n) {
+  const char* force = getenv("PD_TRIDIAG_GTSV");
+  c->use_gtsv = force && atoi(force) != 0;
+  for (int n = 0; n < c->F && !c->use_gtsv; ++n) {
     const cld A = l2[n] * (long double)sub, B = l1[n] + l2[n] * (long double)dia, Cc = l2[n] * (long double)sup;
     const cld D = std::sqrt(B * B - 4.0L * A * Cc);
     cld den1 = -B - D, den2 = -B + D;
@@ -135,13 +165,12 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
     if (std::abs(den) == 0.0L) return fail(c, PD_ESINGULAR, "shifted system n=%d is singular (b = 0, ac = 0)", n);
     const cld tau = 2.0L / den;
     const cld r2 = A * tau, s = Cc * tau;
-    // stability of the two first-order recurrences over the N rows
+    // stability of the two first-order recurrences over the N rows; outside it: the pivoted elimination
     const long double g2 = powl(std::abs(r2), (long double)N), gs = powl(std::abs(s), (long double)N);
-    if (!(g2 < 1e8L) || !(gs < 1e8L))
-      return fail(c, PD_EINVAL,
-                  "shifted system n=%d: characteristic roots |r2|=%.6Lf |1/r1|=%.6Lf outside the stable regime of "
-                  "the recurrence solver",
-                  n, std::abs(r2), std::abs(s));
+    if (!(g2 < 1e8L) || !(gs < 1e8L)) {
+      c->use_gtsv = true;
+      break;
+    }
     // singularity: x_0 = x^(d)_0 / (1 - c q_0),  q_0 = -tau sum_{j<N} s^j r2^{j+1}
     cld q0 = 0.0L, sp = 1.0L, rp = r2;
     for (int j = 0; j < N; ++j) {
@@ -168,6 +197,17 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
     t.sL = d2(sL);
     out[n] = t;
   }
+  if (c->use_gtsv) {
+    for (int n = 0; n < c->F; ++n) {
+      const cld A = l2[n] * (long double)sub, B = l1[n] + l2[n] * (long double)dia, Cc = l2[n] * (long double)sup;
+      const long double mp = gtsv_min_pivot(A, B, Cc, N);
+      if (!(mp > 1e-15L))
+        return fail(c, PD_ESINGULAR,
+                    "shifted system lambda1 I + lambda2 K singular at frequency n=%d (pivoted elimination: min "
+                    "|pivot| / max |entry| = %.3Le)", n, mp);
+      out[n] = pd_tri_coef{};
+    }
+  }
   return PD_OK;
 }
 
@@ -182,7 +222,9 @@ static void free_ctx(pd_ctx* c) {
   if (c->ivp_init) cudaFree(c->ivp_init);
   if (c->ivp_f) cudaFree(c->ivp_f);
   if (c->gm_hflag) cudaFreeHost(c->gm_hflag);
-  if (c->nl_cp) cudaFree(c->nl_cp);
+  if (c->gtsv_scratch) cudaFree(c->gtsv_scratch);
+  if (c->gtsv_bad) cudaFree(c->gtsv_bad);
+  if (c->gtsv_hbad) cudaFreeHost(c->gtsv_hbad);
   void* ptrs[] = {c->tw_n1, c->tw_n2, c->tf4_scratch, c->gam, c->igam, c->tw_t, c->lam1, c->lam2, c->tri, c->sx, c->sn, c->tw_s, c->Sh, c->rvec,
                   c->partial, c->dred, c->zvec, c->stage_a, c->stage_b};
   for (void* p : ptrs)
@@ -263,9 +305,9 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   // dist == NULL or size == 1: single GPU.  rank >= 0: NCCL rank (local slab vectors).  rank < 0: `size`
   // virtual ranks in this process on one GPU (global vectors; the sharded path's test mode).
   c->dist_mode = size > 1 ? (dist->rank < 0 ? 2 : 1) : 0;
-  if (c->dist_mode == 1 && !dist->nccl_id) {
+  if (c->dist_mode == 1 && !dist->nccl_id && !dist->nccl_comm) {
     free_ctx(c);
-    return fail(nullptr, PD_EINVAL, "multi-GPU setup needs an NCCL unique id (pd_nccl_unique_id)");
+    return fail(nullptr, PD_EINVAL, "multi-GPU setup needs an NCCL communicator or unique id (pd_nccl_unique_id)");
   }
   if (c->dist_mode == 1) {
     const pd_plan pl = pd_make_plan(g->op, g->nx, g->ny, nt, size);
@@ -509,7 +551,7 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
       c->npartial *= size;
       SETUP_CUDA(dalloc(&c->partial, (size_t)c->npartial));
     }
-    const pd_status ds = pd_dist_setup(c, dist->nccl_id);
+    const pd_status ds = pd_dist_setup(c, dist->nccl_id, dist->nccl_comm);
     if (ds != PD_OK) {
       std::string m = c->err;
       free_ctx(c);
@@ -607,6 +649,18 @@ static void phase_end(pd_ctx* c, int ph) {
   }
 }
 
+// workspace of the pivoted 1D Step (b) (gtsv.cu), allocated on first use: factors [F][Nx] and the singular flag
+pd_status pd_gtsv_ensure(pd_ctx* c) {
+  if (!c->gtsv_scratch)
+    PD_CUDA(c, cudaMalloc(&c->gtsv_scratch, pd_gtsv_scratch_bytes(c->g.nx, c->F)));
+  if (!c->gtsv_bad) {
+    PD_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->gtsv_bad), sizeof(int)));
+    PD_CUDA(c, cudaMemsetAsync(c->gtsv_bad, 0, sizeof(int), c->st));
+    PD_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->gtsv_hbad), sizeof(int)));
+  }
+  return PD_OK;
+}
+
 // Step (b) on a spectrum buffer holding frequencies [f0, f0 + nfreq) on full spatial rows
 pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   phase_begin(c, 1);
@@ -624,6 +678,10 @@ pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
       PD_CUDA(c, pd_launch_slab2d(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sx, c->sn, c->slab, c->tw_s,
                                   c->slab_chunk, c->use_tfx ? 1 : 0, c->st, &nl));
     c->launches += nl;
+  } else if (c->use_gtsv) {
+    if (pd_status s = pd_gtsv_ensure(c); s != PD_OK) return s;
+    PD_LAUNCH(c, pd_launch_gtsv_shift(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->sten.sub, c->sten.dia,
+                                      c->sten.sup, nullptr, c->gtsv_scratch, c->gtsv_bad, c->st));
   } else {
     PD_LAUNCH(c, pd_launch_tridiag(Sh, c->g.nx, nfreq, c->tri + f0, pd_tridiag_rows_per_thread(), c->st));
   }
@@ -740,9 +798,10 @@ pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
   return PD_OK;
 }
 
-// out = b - A u (b != NULL) or A u; if norm2 != NULL: deterministic ||out||^2 into *norm2 (host, syncs)
+// out = b - A u (b != NULL) or A u; if norm2 != NULL: deterministic ||out||^2 into *norm2 (host, syncs).
+// out == NULL (single GPU, with b and norm2): the norm only, no vector written (timing slot 7, 16 B/dof).
 pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2) {
-  const int ph = b ? 3 : 5;
+  const int ph = b ? (out ? 3 : 7) : 5;
   phase_begin(c, ph);
   if (c->dist_mode != 0) {
     pd_status s = pd_dist_stencil(c, b, u, out, nullptr);  // local sum of squares -> dred[0]

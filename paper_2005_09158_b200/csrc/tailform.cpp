@@ -69,6 +69,8 @@ pd_status tail_setup(pd_ctx* c) {
   auto& T = c->tail;
   if (T.ready) return PD_OK;
   if (c->g.op == PD_WAVE2D_DIRICHLET) return fail(c, PD_EINVAL, "tail form: not built for the 2D Dirichlet operator");
+  if (c->use_gtsv)
+    return fail(c, PD_EINVAL, "tail form: the 1D tail map needs the recurrence Step (b) (context uses pivoted elimination)");
   const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
   if (c->nt < 2 * H) return fail(c, PD_EINVAL, "tail form needs Nt >= %d", 2 * H);
   const int nt = c->nt, F = c->F;

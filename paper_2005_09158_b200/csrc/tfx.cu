@@ -20,6 +20,8 @@
 //   inverse  stage 2 (tf4_stages.cuh): N2-point IFFTs over n2, Gamma^{-1}/Nt, real columns out.
 // A stage-2 / inverse stage-1 tile is one full x-row (NX/2 pairs) x 16 rows of length NX/2: 8 NX complex.
 // All transforms are unnormalised (the slab column pass scales by 1/N^2, as before).
+#include <cstdlib>
+
 #include "kernels.h"
 #include "tf4_stages.cuh"
 
@@ -447,6 +449,7 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
   set_attrs<NT, NX>();
   const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
   const bool vec = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
+  const bool tma = !comb && pd_tf4_tma_supported(NT, S, r);
   const long long npairs = S / 2;
   int n = 0;
   if (cudaError_t e = ov_fork(ov, st0)) return e;
@@ -456,9 +459,11 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
     double2* scratch = lane ? ov->scratch[lane] : scratch0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
     const dim3 g1((unsigned)((pc + KP - 1) / KP), kN1), g2((unsigned)(pc / NP), N2 / 2 + 1);
-    if (comb)
+    if (comb) {
       tf4_fwd_s1_comb<NT, N2, KP, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(*comb, S, p, pc, scratch, gam, tb.tw2, tb.twt);
-    else if (vec)
+    } else if (tma) {
+      if (cudaError_t e = pd_launch_tf4_fwd_s1_tma(NT, r, S, p, pc, scratch, gam, tb.tw2, tb.twt, st)) return e;
+    } else if (vec)
       tf4_fwd_s1<NT, N2, KP, true, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
     else
       tf4_fwd_s1<NT, N2, KP, false, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
@@ -514,10 +519,13 @@ cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, c
 
 }  // namespace
 
-// Nt <= 512: the single-tile time FFT plus the three-launch slab solve measured faster on B200 (cfg3).
+// Nt = 256 / 512 too since r02: with the y-pass by cyclic Toeplitz solves the fold wins at cfg3 (apply 0.283 ->
+// 0.230 ms: the slab x-FFT row passes leave Step (b)); PD_TFX_SMALL=0 restores the single-tile FFT + row passes.
 // NX = 1024 (instantiated, not parity-tested: Nt >= 1024 makes it 1e9 dofs) takes the tf4 + slab route.
 int pd_tfx_supported(int nt, int nx) {
-  const bool t = nt == 1024 || nt == 2048 || nt == 4096;
+  const char* se = getenv("PD_TFX_SMALL");
+  const bool small = se == nullptr || atoi(se) != 0;
+  const bool t = nt == 1024 || nt == 2048 || nt == 4096 || (small && (nt == 256 || nt == 512));
   const bool x = nx == 32 || nx == 64 || nx == 128 || nx == 256 || nx == 512;
   return t && x;
 }
@@ -537,6 +545,7 @@ long long pd_tfx_chunk_align(int nt, int nx) {
   case T * 10000 + 1024: return FN<T, 1024> ARGS;
 #define PD_TFX_SWITCH(FN, ARGS)                                                                      \
   switch (nt * 10000 + nx) {                                                                         \
+    PD_TFX_ROW(256, FN, ARGS) PD_TFX_ROW(512, FN, ARGS)                                              \
     PD_TFX_ROW(1024, FN, ARGS) PD_TFX_ROW(2048, FN, ARGS) PD_TFX_ROW(4096, FN, ARGS)                 \
     default: return cudaErrorInvalidValue;                                                           \
   }
