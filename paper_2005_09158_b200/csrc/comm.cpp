@@ -28,6 +28,7 @@ struct Api {
   ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
 };
 
@@ -59,6 +60,7 @@ bool load() {
   PD_SYM(send, "ncclSend")
   PD_SYM(recv, "ncclRecv")
   PD_SYM(allReduce, "ncclAllReduce")
+  PD_SYM(allGather, "ncclAllGather")
   PD_SYM(errStr, "ncclGetErrorString")
 #undef PD_SYM
   return true;
@@ -136,4 +138,8 @@ int pd_comm_recv(pd_comm* c, void* buf, size_t bytes, int peer) {
 
 int pd_comm_allreduce_sum(pd_comm* c, double* d, int n) {
   return check(g_api.allReduce(d, d, (size_t)n, kNcclFloat64, kNcclSum, c->comm, c->st), "ncclAllReduce");
+}
+
+int pd_comm_allgather(pd_comm* c, const void* send, void* recv, size_t bytes) {
+  return check(g_api.allGather(send, recv, bytes, kNcclInt8, c->comm, c->st), "ncclAllGather");
 }

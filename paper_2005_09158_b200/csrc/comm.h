@@ -18,3 +18,5 @@ int pd_comm_group_end(pd_comm* c);
 int pd_comm_send(pd_comm* c, const void* buf, size_t bytes, int peer);
 int pd_comm_recv(pd_comm* c, void* buf, size_t bytes, int peer);
 int pd_comm_allreduce_sum(pd_comm* c, double* d, int n);
+// recv[q * bytes ...] = send of rank q (device buffers, stream-ordered)
+int pd_comm_allgather(pd_comm* c, const void* send, void* recv, size_t bytes);

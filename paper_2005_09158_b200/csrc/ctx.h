@@ -30,7 +30,8 @@ struct pd_shard {
   int F = 0, f0 = 0;          // local frequencies
   double2* Sh_loc = nullptr;  // [F_all][S]  all frequencies of the local slab
   double2* Sg = nullptr;      // [F][S_glob] local frequencies of every spatial dof
-  double2* stage = nullptr;   // NCCL receive/send staging
+  double2* stage = nullptr;   // NCCL receive/send staging (fallback exchange when peer mappings are unavailable)
+  double2* peer[kPdMaxRanks] = {};  // NCCL ranks with P2P: rank q's Sg mapped into this process (CUDA IPC)
   double* hlo = nullptr;      // halos [Nt][hw]
   double* hhi = nullptr;
   double* h1lo = nullptr;     // single-level halos for the rhs (u0, v0): [2][hw]
@@ -54,6 +55,7 @@ struct pd_ctx {
   // process on one GPU (global vectors, exchanges by device copies; test mode for the sharded path)
   int rank = 0, size = 1, dist_mode = 0;
   pd_comm* comm = nullptr;
+  bool p2p = false;              // mode 1: Step (a) / (c) read and write the owners' Sg through NVLink peer mappings
   std::vector<pd_shard> shards;  // modes 1 (one entry: this rank) and 2 (all virtual ranks)
   pd_plan plan;
   int nx_loc = 0, ny_loc = 0;    // local spatial extent (1D: x-range, 2D: y-rows)
@@ -105,6 +107,7 @@ struct pd_ctx {
   std::vector<double*> V;
   double* zvec = nullptr;
   double* gm_head = nullptr;     // head-sized work vector of the corner-identity GMRES path
+  double* gm_full = nullptr;     // NCCL ranks: replicated [H][S_glob] tail and head of the corner identity
   int* gm_flag = nullptr;        // zero-initial-guess check
   double* ivp_init = nullptr;    // pd_solve_ivp_host: u0, v0 on the device
   double* ivp_f = nullptr;       // pd_solve_ivp_host: source samples
@@ -183,7 +186,9 @@ pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double*
 extern "C" void pd_report_push(pd_report* rep, double v);
 void pd_tail_free(pd_ctx* c);
 void pd_corner_coefs(const pd_ctx* c, pd_tail_g* gc);
+pd_status pd_corner_head(pd_ctx* c, const pd_tail_g& gc, const double* tail, double* head);
 pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0);
 pd_status pd_gtsv_ensure(pd_ctx* c);
-pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S);
-pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate);
+// Steps (a) / (c) of a local slab [Nt][S]; the spectrum rows through sp (pd_spec_local(c->Sh, S) on one GPU)
+pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, const pd_spec& sp, long long S);
+pd_status pd_time_fft_inv(pd_ctx* c, const pd_spec& sp, double* z, long long S, int accumulate);

@@ -3,18 +3,23 @@
 // transposed back").
 //
 //   rank p owns the spatial slab [off_p, off_p + S_p) for all Nt time levels (1D: x-range, 2D: y-rows)
-//   Step (a)  local time FFT of the slab -> Sh_loc[F][S_p]                    (no communication)
-//   all-to-all: block (frequencies of q) x (dofs of p) goes p -> q: contiguous rows [f_q, f_q+F_q) of
-//               Sh_loc on the sender, a pitched column block of Sg_q[F_q][S_glob] on the receiver
+//   Step (a)  time FFT of the slab; frequency row n goes to its owner q: columns [off_p, +S_p) of Sg_q[F_q][S_glob]
+//   all-to-all: block (frequencies of q) x (dofs of p) goes p -> q (fused into Step (a), see below)
 //   Step (b)  spatial solves of the F_q local frequencies on full spatial rows   (no communication)
 //   all-to-all back, Step (c) local inverse time FFT
 //   residual: one halo column (1D) / row (2D, periodic ring) per side and time level from the neighbours
 //
-// One exchange plan, two executors: dist_mode 1 runs it over NCCL (grouped ncclSend/ncclRecv, receive
-// into staging + one pitched device copy per block); dist_mode 2 runs P virtual ranks of this process on
-// one GPU, moving every block with the same pitched device copies, so the sharded path is parity-tested
-// on a single B200 (tests/test_gpu_dist.py).  Plan logic is host-only (pd_make_plan) and covered by the
-// world-size-2 gloo test (tests/test_dist_plan.py).
+// The all-to-alls are fused into the time-FFT kernels: Step (a)'s epilogue stores each frequency row straight into
+// its owner's Step (b) buffer Sg_q[F_q][S_glob] (at this slab's columns), and Step (c)'s prologue loads it back from
+// there (pd_spec in kernels.h): no staging buffer, no copy pass.  The owners' buffers are
+//   dist_mode 2: P virtual ranks of this process on one GPU (plain device pointers) - the sharded path's GPU test
+//                mode (tests/test_gpu_dist.py), running the very kernels and views of mode 1;
+//   dist_mode 1: NCCL ranks, one GPU each: every Sg is exported with CUDA IPC, the handles all-gathered over NCCL and
+//                opened as peer mappings (NVLink); two stream-ordered NCCL barriers per apply separate the writers of
+//                Step (a) from the Step (b) readers and Step (b) from the Step (c) readers.  If the peer mappings
+//                cannot be opened (no P2P path, > kPdMaxRanks ranks), the plan runs as grouped ncclSend/ncclRecv
+//                into a staging buffer plus one pitched copy per block (the fallback exchange).
+// Plan logic is host-only (pd_make_plan) and covered by the world-size-2 gloo test (tests/test_dist_plan.py).
 #include <algorithm>
 #include <cstring>
 
@@ -66,6 +71,51 @@ extern "C" pd_status pd_partition(int op, int nx, int ny, int nt, int size, long
 
 static int hw_of(const pd_ctx* c) { return pd_is_2d(c->g.op) ? c->g.nx : 1; }
 
+// mode 1: export this rank's Sg, all-gather the IPC handles over NCCL, open every peer's (c->p2p on success; any
+// failure leaves the fallback exchange in place)
+static void open_peers(pd_ctx* c) {
+  pd_shard& me = c->shards[0];
+  const int P = c->size;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, me.Sg) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  char* dbuf = nullptr;
+  std::vector<cudaIpcMemHandle_t> all(P);
+  bool ok = cudaMalloc(&dbuf, sizeof(h) * (P + 1)) == cudaSuccess;
+  ok = ok && cudaMemcpy(dbuf + sizeof(h) * P, &h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && pd_comm_allgather(c->comm, dbuf + sizeof(h) * P, dbuf, sizeof(h)) == 0;
+  ok = ok && cudaStreamSynchronize(c->st) == cudaSuccess;
+  ok = ok && cudaMemcpy(all.data(), dbuf, sizeof(h) * P, cudaMemcpyDeviceToHost) == cudaSuccess;
+  if (dbuf) cudaFree(dbuf);
+  for (int q = 0; ok && q < P; ++q) {
+    if (q == c->rank) continue;
+    void* ptr = nullptr;
+    ok = cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    me.peer[q] = static_cast<double2*>(ptr);
+  }
+  // every rank must take the same route: agree on the outcome (min over ranks)
+  double flag = ok ? 1.0 : 0.0, *dflag = nullptr;
+  if (cudaMalloc(&dflag, sizeof(double)) == cudaSuccess) {
+    cudaMemcpy(dflag, &flag, sizeof(double), cudaMemcpyHostToDevice);
+    flag = (pd_comm_allreduce_sum(c->comm, dflag, 1) == 0 && cudaStreamSynchronize(c->st) == cudaSuccess &&
+            cudaMemcpy(&flag, dflag, sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess)
+               ? flag
+               : 0.0;
+    cudaFree(dflag);
+  } else {
+    flag = 0.0;
+  }
+  c->p2p = ok && flag == (double)P;
+  if (!c->p2p) {
+    for (int q = 0; q < P; ++q)
+      if (me.peer[q]) cudaIpcCloseMemHandle(me.peer[q]);
+    for (auto& p : me.peer) p = nullptr;
+    cudaGetLastError();
+  }
+}
+
 pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id, void* nccl_comm) {
   const int P = c->size;
   c->plan = pd_make_plan(c->g.op, c->g.nx, c->g.ny, c->nt, P);
@@ -108,8 +158,7 @@ pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id, void* nccl_comm) {
       if (e == cudaSuccess) e = dalloc(&sh.sendlo, (size_t)c->nt * hw);
       if (e == cudaSuccess) e = dalloc(&sh.sendhi, (size_t)c->nt * hw);
     } else {
-      e = dalloc(&sh.Sh_loc, (size_t)c->F * sh.S);
-      if (e == cudaSuccess) e = dalloc(&sh.r_loc, (size_t)(c->nt + 1) * sh.S);
+      e = dalloc(&sh.r_loc, (size_t)(c->nt + 1) * sh.S);
       if (e == cudaSuccess) e = dalloc(&sh.z_loc, (size_t)(c->nt + 1) * sh.S);
       if (e == cudaSuccess) e = dalloc(&sh.b_loc, (size_t)(c->nt + 1) * sh.S);
     }
@@ -122,16 +171,21 @@ pd_status pd_dist_setup(pd_ctx* c, const void* nccl_id, void* nccl_comm) {
     if (e != cudaSuccess) return fail(c, PD_ENOMEM, "sharded workspace: %s", cudaGetErrorString(e));
   }
   (void)maxS;
+  if (c->dist_mode == 1 && P <= kPdMaxRanks && getenv("PD_NO_P2P") == nullptr) open_peers(c);
   return PD_OK;
 }
 
 void pd_dist_free(pd_ctx* c) {
   for (pd_shard& sh : c->shards) {
+    for (double2*& p : sh.peer)
+      if (p) {
+        cudaIpcCloseMemHandle(p);
+        p = nullptr;
+      }
     void* ptrs[] = {sh.Sg, sh.stage, sh.hlo, sh.hhi, sh.h1lo, sh.h1hi, sh.sendlo, sh.sendhi, sh.r_loc, sh.z_loc,
                     sh.b_loc};
     for (void* p : ptrs)
       if (p) cudaFree(p);
-    if (c->dist_mode == 2 && sh.Sh_loc) cudaFree(sh.Sh_loc);
   }
   c->shards.clear();
 }
@@ -146,16 +200,17 @@ static cudaError_t scatter(const pd_ctx* c, const pd_shard& sh, const double* lo
                            rows, cudaMemcpyDeviceToDevice, c->st);
 }
 
-// block (frequencies of q) x (dofs of p): rows [f_q, f_q + F_q) of Sh_loc_p  <->  columns [off_p, +S_p) of Sg_q
-static cudaError_t block_fwd(const pd_ctx* c, const pd_shard& src_p, const pd_shard& dst_q) {
-  return cudaMemcpy2DAsync(dst_q.Sg + src_p.off, c->Sg * sizeof(double2), src_p.Sh_loc + (long long)dst_q.f0 * src_p.S,
-                           src_p.S * sizeof(double2), src_p.S * sizeof(double2), dst_q.F, cudaMemcpyDeviceToDevice,
-                           c->st);
-}
-static cudaError_t block_bwd(const pd_ctx* c, const pd_shard& src_q, const pd_shard& dst_p) {
-  return cudaMemcpy2DAsync(dst_p.Sh_loc + (long long)src_q.f0 * dst_p.S, dst_p.S * sizeof(double2),
-                           src_q.Sg + dst_p.off, c->Sg * sizeof(double2), dst_p.S * sizeof(double2), src_q.F,
-                           cudaMemcpyDeviceToDevice, c->st);
+// spectrum view of shard `sh`: frequency rows of owner q at Sg_q + (n - f_q) S_glob, this slab's columns
+static pd_spec spec_of(const pd_ctx* c, const pd_shard& sh) {
+  pd_spec v{};
+  v.P = c->size;
+  v.pitch = c->Sg;
+  for (int q = 0; q < c->size; ++q) {
+    double2* owner = c->dist_mode == 2 ? c->shards[q].Sg : (q == c->rank ? sh.Sg : sh.peer[q]);
+    v.base[q] = owner + sh.off;
+    v.f0[q] = c->plan.f_off[q];
+  }
+  return v;
 }
 
 #define PD_NCCL(ctx, expr) \
@@ -163,13 +218,17 @@ static cudaError_t block_bwd(const pd_ctx* c, const pd_shard& src_q, const pd_sh
     if ((expr) != 0) return fail(ctx, PD_ENCCL, "%s: %s", #expr, pd_comm_last_error()); \
   } while (0)
 
+// fallback exchange (mode 1 without peer mappings): grouped ncclSend / ncclRecv into staging + pitched copies
+static cudaError_t block_self(const pd_ctx* c, const pd_shard& me, bool fwd) {
+  if (fwd)
+    return cudaMemcpy2DAsync(me.Sg + me.off, c->Sg * sizeof(double2), me.Sh_loc + (long long)me.f0 * me.S,
+                             me.S * sizeof(double2), me.S * sizeof(double2), me.F, cudaMemcpyDeviceToDevice, c->st);
+  return cudaMemcpy2DAsync(me.Sh_loc + (long long)me.f0 * me.S, me.S * sizeof(double2), me.Sg + me.off,
+                           c->Sg * sizeof(double2), me.S * sizeof(double2), me.F, cudaMemcpyDeviceToDevice, c->st);
+}
+
 static pd_status exchange_fwd(pd_ctx* c) {
   const pd_plan& pl = c->plan;
-  if (c->dist_mode == 2) {
-    for (const pd_shard& q : c->shards)
-      for (const pd_shard& p : c->shards) PD_CUDA(c, block_fwd(c, p, q));
-    return PD_OK;
-  }
   pd_shard& me = c->shards[0];
   const int P = c->size, r = me.rank;
   PD_NCCL(c, pd_comm_group_start(c->comm));
@@ -184,7 +243,7 @@ static pd_status exchange_fwd(pd_ctx* c) {
                             p));
   }
   PD_NCCL(c, pd_comm_group_end(c->comm));
-  PD_CUDA(c, block_fwd(c, me, me));
+  PD_CUDA(c, block_self(c, me, true));
   for (int p = 0; p < P; ++p) {
     if (p == r) continue;
     PD_CUDA(c, cudaMemcpy2DAsync(me.Sg + pl.s_off[p], c->Sg * sizeof(double2), me.stage + (long long)me.F * pl.s_off[p],
@@ -196,11 +255,6 @@ static pd_status exchange_fwd(pd_ctx* c) {
 
 static pd_status exchange_bwd(pd_ctx* c) {
   const pd_plan& pl = c->plan;
-  if (c->dist_mode == 2) {
-    for (const pd_shard& q : c->shards)
-      for (const pd_shard& p : c->shards) PD_CUDA(c, block_bwd(c, q, p));
-    return PD_OK;
-  }
   pd_shard& me = c->shards[0];
   const int P = c->size, r = me.rank;
   for (int p = 0; p < P; ++p) {
@@ -209,7 +263,7 @@ static pd_status exchange_bwd(pd_ctx* c) {
                                  me.Sg + pl.s_off[p], c->Sg * sizeof(double2), pl.s_cnt[p] * sizeof(double2), me.F,
                                  cudaMemcpyDeviceToDevice, c->st));
   }
-  PD_CUDA(c, block_bwd(c, me, me));
+  PD_CUDA(c, block_self(c, me, false));
   PD_NCCL(c, pd_comm_group_start(c->comm));
   for (int p = 0; p < P; ++p) {
     if (p == r) continue;
@@ -225,24 +279,33 @@ static pd_status exchange_bwd(pd_ctx* c) {
   return PD_OK;
 }
 
+// stream-ordered barrier over the NCCL ranks (a one-double all-reduce): the peer stores of the kernels before it are
+// complete on every rank when it completes
+static pd_status rank_barrier(pd_ctx* c) {
+  if (pd_comm_allreduce_sum(c->comm, c->dred + 63, 1) != 0)
+    return fail(c, PD_ENCCL, "barrier allreduce: %s", pd_comm_last_error());
+  return PD_OK;
+}
+
 pd_status pd_dist_apply(pd_ctx* c, const double* r, double* z, int accumulate) {
   pd_status s;
+  const bool fused = c->dist_mode == 2 || c->p2p;  // the all-to-alls inside the time-FFT kernels
   for (pd_shard& sh : c->shards) {
     const double* rin = r;
     if (c->dist_mode == 2) {
       PD_CUDA(c, gather(c, sh, r, sh.r_loc, c->nt));
       rin = sh.r_loc;
     }
-    s = pd_time_fft_fwd(c, rin, sh.Sh_loc, sh.S);
+    s = pd_time_fft_fwd(c, rin, fused ? spec_of(c, sh) : pd_spec_local(sh.Sh_loc, sh.S), sh.S);
     if (s != PD_OK) return s;
   }
-  s = exchange_fwd(c);
+  s = fused ? (c->dist_mode == 1 ? rank_barrier(c) : PD_OK) : exchange_fwd(c);
   if (s != PD_OK) return s;
   for (pd_shard& sh : c->shards) {
     s = pd_spatial_solve(c, sh.Sg, sh.F, sh.f0);
     if (s != PD_OK) return s;
   }
-  s = exchange_bwd(c);
+  s = fused ? (c->dist_mode == 1 ? rank_barrier(c) : PD_OK) : exchange_bwd(c);
   if (s != PD_OK) return s;
   for (pd_shard& sh : c->shards) {
     double* out = z;
@@ -250,7 +313,7 @@ pd_status pd_dist_apply(pd_ctx* c, const double* r, double* z, int accumulate) {
       if (accumulate) PD_CUDA(c, gather(c, sh, z, sh.z_loc, c->nt));
       out = sh.z_loc;
     }
-    s = pd_time_fft_inv(c, sh.Sh_loc, out, sh.S, accumulate);
+    s = pd_time_fft_inv(c, fused ? spec_of(c, sh) : pd_spec_local(sh.Sh_loc, sh.S), out, sh.S, accumulate);
     if (s != PD_OK) return s;
     if (c->dist_mode == 2) PD_CUDA(c, scatter(c, sh, sh.z_loc, z, c->nt));
   }

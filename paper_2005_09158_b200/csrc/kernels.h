@@ -2,11 +2,42 @@
 #pragma once
 #include <cuda_runtime.h>
 
+// ---- where row n of the half spectrum lives (the output of Step (a), the input of Step (c)) ----
+// Single GPU: one owner, base[0] = Sh, pitch = S.  Sharded (dist.cpp): the frequencies [f0[q], f0[q + 1]) belong to
+// rank q, whose Step (b) buffer holds them on full spatial rows (pitch = S_glob); base[q] points at this slab's first
+// column in it (device memory of this process for virtual ranks, a CUDA-IPC mapping of the peer's buffer over
+// NVLink for NCCL ranks).  Step (a)'s stores and Step (c)'s loads then go straight to / from the owner: the
+// space -> frequency all-to-all is the time-FFT kernels' own epilogue (and frequency -> space their prologue).
+constexpr int kPdMaxRanks = 8;
+struct pd_spec {
+  double2* base[kPdMaxRanks];
+  int f0[kPdMaxRanks];
+  int P;
+  long long pitch;
+};
+// SH = false (single GPU): base[0] + n pitch, no owner lookup (the kernels are instantiated for both)
+template <bool SH = true>
+__host__ __device__ __forceinline__ double2* pd_spec_row(const pd_spec& v, int n) {
+  if (!SH) return v.base[0] + (long long)n * v.pitch;
+  int q = 0;
+#pragma unroll
+  for (int i = 1; i < kPdMaxRanks; ++i) q += (i < v.P && n >= v.f0[i]) ? 1 : 0;
+  return v.base[q] + (long long)(n - v.f0[q]) * v.pitch;
+}
+inline pd_spec pd_spec_local(const double2* Sh, long long S) {
+  pd_spec v{};
+  v.base[0] = const_cast<double2*>(Sh);
+  v.P = 1;
+  v.pitch = S;
+  return v;
+}
+
 // ---- Steps (a)/(c): time-axis FFTs (tfft.cu) ----
 int pd_tfft_supported(int nt);
-cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+// r / z: [Nt][S] real (row stride S), spectrum rows through sp (columns [0, S) of each row)
+cudaError_t pd_launch_tfft_fwd(int nt, const double* r, const pd_spec& sp, long long S, const double* gam,
                                const double2* tw, cudaStream_t st);
-cudaError_t pd_launch_tfft_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+cudaError_t pd_launch_tfft_inv(int nt, const pd_spec& sp, double* z, long long S, const double* igam,
                                const double2* tw, int accumulate, cudaStream_t st);
 
 // ---- Steps (a)/(c) for Nt >= 1024: four-step time FFT with an L2-resident scratch (tfft4.cu) ----
@@ -27,10 +58,10 @@ struct pd_comb_args {
   double c[kPdCombMax];
   int k;
 };
-cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+cudaError_t pd_launch_tf4_fwd(int nt, const double* r, const pd_spec& sp, long long S, const double* gam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
                               int* nl, const pd_tfx_overlap* ov = nullptr);
-cudaError_t pd_launch_tf4_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+cudaError_t pd_launch_tf4_inv(int nt, const pd_spec& sp, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, int accumulate,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);
 
@@ -93,11 +124,11 @@ int pd_tf4_tma_supported(int nt, long long S, const void* r);
 cudaError_t pd_launch_tf4_fwd_s1_tma(int nt, const double* r, long long S, long long p_begin, long long pc,
                                      double2* Y, const double* gam, const double2* tw2, const double2* twt,
                                      cudaStream_t st);
-cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
+cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, const pd_spec& sp, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr,
                               const pd_comb_args* comb = nullptr);  // comb: r unused
-cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
+cudaError_t pd_launch_tfx_inv(int nt, int nx, const pd_spec& sp, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               int accumulate, cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);
 

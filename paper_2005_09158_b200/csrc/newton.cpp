@@ -59,11 +59,11 @@ pd_status pd_solve_newton(pd_ctx* c, const double* b, double* u, double tol, int
     }
     if (rel <= tol || k >= maxit) break;
     PD_LAUNCH(c, pd_launch_jac_avg(u, c->nl_dbar, c->nt, c->S, c->sten.g3, c->sten.g1, c->st));
-    s = pd_time_fft_fwd(c, c->rvec, c->Sh, c->S);  // Step (a)
+    s = pd_time_fft_fwd(c, c->rvec, pd_spec_local(c->Sh, c->S), c->S);  // Step (a)
     if (s != PD_OK) return s;
     PD_LAUNCH(c, pd_launch_gtsv_shift(c->Sh, c->g.nx, c->F, c->lam1, c->lam2, c->sten.sub, c->sten.dia, c->sten.sup,
                                       c->nl_dbar, c->gtsv_scratch, c->gtsv_bad, c->st));  // Step (b), J = K + diag(dbar)
-    s = pd_time_fft_inv(c, c->Sh, u, c->S, 1);  // Step (c) fused with u += du
+    s = pd_time_fft_inv(c, pd_spec_local(c->Sh, c->S), u, c->S, 1);  // Step (c) fused with u += du
     if (s != PD_OK) return s;
     ++k;
   }

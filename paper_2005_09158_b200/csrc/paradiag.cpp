@@ -218,6 +218,7 @@ static void free_ctx(pd_ctx* c) {
   if (c->mu) cudaFree(c->mu);
   if (c->nl_dbar) cudaFree(c->nl_dbar);
   if (c->gm_head) cudaFree(c->gm_head);
+  if (c->gm_full) cudaFree(c->gm_full);
   if (c->gm_flag) cudaFree(c->gm_flag);
   if (c->ivp_init) cudaFree(c->ivp_init);
   if (c->ivp_f) cudaFree(c->ivp_f);
@@ -690,21 +691,21 @@ pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
 }
 
 // Step (a) of a local slab: r [Nt][S] -> Sh [F][S]
-pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, double2* Sh, long long S) {
+pd_status pd_time_fft_fwd(pd_ctx* c, const double* r, const pd_spec& sp, long long S) {
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   phase_begin(c, 0);
   if (c->use_tfx) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, Sh, S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
+    PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, sp, S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
                                  c->ov.k > 1 ? &c->ov : nullptr));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, Sh, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
+    PD_CUDA(c, pd_launch_tf4_fwd(c->nt, r, sp, S, c->gam, tb, c->tf4_scratch, c->tf4_chunk, c->st, &nl,
                                  c->ov.k > 1 ? &c->ov : nullptr));
     c->launches += nl;
   } else {
-    PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, Sh, S, c->gam, c->tw_t, c->st));
+    PD_LAUNCH(c, pd_launch_tfft_fwd(c->nt, r, sp, S, c->gam, c->tw_t, c->st));
   }
   phase_end(c, 0);
   return PD_OK;
@@ -718,22 +719,22 @@ static const pd_tfx_overlap* inv_view(const pd_ctx* c, int accumulate) {
 }
 
 // Step (c) of a local slab: Sh [F][S] -> z [Nt][S] (z += when accumulate)
-pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, int accumulate) {
+pd_status pd_time_fft_inv(pd_ctx* c, const pd_spec& sp, double* z, long long S, int accumulate) {
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   const int ph = accumulate ? 4 : 2;
   phase_begin(c, ph);
   if (c->use_tfx) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tfx_inv(c->nt, c->g.nx, Sh, z, S, c->igam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
+    PD_CUDA(c, pd_launch_tfx_inv(c->nt, c->g.nx, sp, z, S, c->igam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
                                  accumulate, c->st, &nl, inv_view(c, accumulate)));
     c->launches += nl;
   } else if (c->use_tf4) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_tf4_inv(c->nt, Sh, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl,
+    PD_CUDA(c, pd_launch_tf4_inv(c->nt, sp, z, S, c->igam, tb, c->tf4_scratch, c->tf4_chunk, accumulate, c->st, &nl,
                                  inv_view(c, accumulate)));
     c->launches += nl;
   } else {
-    PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, Sh, z, S, c->igam, c->tw_t, accumulate, c->st));
+    PD_LAUNCH(c, pd_launch_tfft_inv(c->nt, sp, z, S, c->igam, c->tw_t, accumulate, c->st));
   }
   phase_end(c, ph);
   return PD_OK;
@@ -741,11 +742,12 @@ pd_status pd_time_fft_inv(pd_ctx* c, const double2* Sh, double* z, long long S, 
 
 static pd_status apply_direct(pd_ctx* c, const double* r, double* z, int accumulate) {
   if (c->dist_mode != 0) return pd_dist_apply(c, r, z, accumulate);
-  pd_status s = pd_time_fft_fwd(c, r, c->Sh, c->S);
+  const pd_spec sp = pd_spec_local(c->Sh, c->S);
+  pd_status s = pd_time_fft_fwd(c, r, sp, c->S);
   if (s != PD_OK) return s;
   s = pd_spatial_solve(c, c->Sh, c->F, 0);
   if (s != PD_OK) return s;
-  return pd_time_fft_inv(c, c->Sh, z, c->S, accumulate);
+  return pd_time_fft_inv(c, sp, z, c->S, accumulate);
 }
 
 // u += P^{-1} (sum_i cb.c[i] cb.x[i]) with the combination read by the forward time FFT's stage-1 loader (tfx path,
@@ -755,13 +757,13 @@ static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double
   const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
   phase_begin(c, 6);
   int nl = 0;
-  PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, nullptr, c->Sh, c->S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
+  PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, nullptr, pd_spec_local(c->Sh, c->S), c->S, c->gam, tb, c->tw_s, c->tf4_scratch, c->tf4_chunk,
                                c->st, &nl, c->ov.k > 1 ? &c->ov : nullptr, cb));
   c->launches += nl;
   phase_end(c, 6);
   pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
   if (s != PD_OK) return s;
-  return pd_time_fft_inv(c, c->Sh, u, c->S, accumulate);
+  return pd_time_fft_inv(c, pd_spec_local(c->Sh, c->S), u, c->S, accumulate);
 }
 
 // z = P^{-1} r, or u += P^{-1} r when accumulate.  With graphs enabled (single GPU, phase timing off) the
@@ -920,6 +922,33 @@ pd_status pd_solve_stationary(pd_ctx* c, const double* b, double* u, double tol,
   return conv ? PD_OK : PD_NOT_CONVERGED;
 }
 
+// head = G tail: the (P_alpha - A) block rows of the corner identity from the last H time blocks of a local vector.
+// NCCL ranks: the tails are replicated (zero-padded copy + sum all-reduce of H S_glob doubles), G is applied on the
+// global grid (no halos needed) and the local columns are kept.
+extern "C++" pd_status pd_corner_head(pd_ctx* c, const pd_tail_g& gc, const double* tail, double* head) {
+  if (c->dist_mode != 1) {
+    PD_LAUNCH(c, pd_launch_head_G(c->sten, gc, tail, head, c->S, c->st));
+    return PD_OK;
+  }
+  const long long Sg = c->Sg, hn = (long long)gc.H * Sg;
+  if (!c->gm_full) PD_CUDA(c, dalloc(&c->gm_full, (size_t)(2 * hn + 2)));
+  double *ft = c->gm_full, *fh = c->gm_full + hn;
+  PD_CUDA(c, cudaMemsetAsync(ft, 0, sizeof(double) * hn, c->st));
+  for (int t = 0; t < gc.H; ++t)
+    PD_CUDA(c, cudaMemcpyAsync(ft + t * Sg + c->off, tail + (long long)t * c->S, sizeof(double) * c->S,
+                               cudaMemcpyDeviceToDevice, c->st));
+  if (pd_comm_allreduce_sum(c->comm, ft, (int)hn) != 0) return fail(c, PD_ENCCL, "allreduce: %s", pd_comm_last_error());
+  pd_stencil gs = c->sten;
+  gs.nx = c->g.nx;
+  gs.ny = c->g.ny;
+  gs.hlo = gs.hhi = nullptr;
+  PD_LAUNCH(c, pd_launch_head_G(gs, gc, ft, fh, Sg, c->st));
+  for (int t = 0; t < gc.H; ++t)
+    PD_CUDA(c, cudaMemcpyAsync(head + (long long)t * c->S, fh + t * Sg + c->off, sizeof(double) * c->S,
+                               cudaMemcpyDeviceToDevice, c->st));
+  return PD_OK;
+}
+
 // zero_guess: u is output only (not read; no zero-check sweep); otherwise u is the initial guess
 static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, int m, int maxit, pd_report* rep,
                             bool zero_guess) {
@@ -997,8 +1026,10 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
   // corner identity path (single GPU, linear operator); PD_GMRES_MATVEC=1 keeps the explicit matvec
   pd_tail_g gcorner{};
   pd_corner_coefs(c, &gcorner);
-  const bool corner = c->dist_mode == 0 && c->sten.g3 == 0.0 && c->sten.g1 == 0.0 && gcorner.H >= 1 &&
-                      c->nt >= 2 * gcorner.H && getenv("PD_GMRES_MATVEC") == nullptr;
+  // sharded contexts too: virtual ranks hold global vectors; NCCL ranks replicate the H tail blocks (one all-reduce
+  // of H S_glob doubles) and form the head on the global grid (pd_corner_head)
+  const bool corner = c->sten.g3 == 0.0 && c->sten.g1 == 0.0 && gcorner.H >= 1 && c->nt >= 2 * gcorner.H &&
+                      getenv("PD_GMRES_MATVEC") == nullptr;
   const long long hn_len = (long long)gcorner.H * c->S;
   std::vector<double> eh(m + 1);
   double ww_known = -1.0;                 // ||w||^2 when the second CGS pass is skipped
@@ -1025,8 +1056,8 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
         // behind the tail form): the matvec sweep disappears and, the basis being orthonormal, the first CGS pass is
         // h_i = delta_ij - sc_i sc_j <X_i[head], G tail>: head-only dots.  The second pass measures the true
         // projections of the assembled w as before, so orthogonality is enforced to working precision.
-        PD_LAUNCH(c, pd_launch_head_G(c->sten, gcorner, c->zvec + (long long)(c->nt - gcorner.H) * c->S, dhead,
-                                      c->S, c->st));
+        s = pd_corner_head(c, gcorner, c->zvec + (long long)(c->nt - gcorner.H) * c->S, dhead);
+        if (s != PD_OK) return s;
         s = pd_krylov_n(c, 0, Xp, nullptr, j + 1, 0.0, dhead, hn_len, eh.data());  // <X_i[head], G tail>
         if (s != PD_OK) return s;
         for (int i = 0; i <= j; ++i) {

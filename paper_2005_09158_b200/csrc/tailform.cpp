@@ -250,7 +250,7 @@ pd_status apply_head(pd_ctx* c, const double* g, double* u, int acc) {
   if (c->use_tfx) PD_LAUNCH(c, pd_launch_slab2d_rows(T.gx, c->g.nx, (long long)T.H * c->g.ny, 0, c->tw_s, c->st));
   PD_LAUNCH(c, pd_launch_head_broadcast(c->Sh, c->F, c->S, T.H, T.hc, T.gx, c->st));
   pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
-  return s != PD_OK ? s : pd_time_fft_inv(c, c->Sh, u, c->S, acc);
+  return s != PD_OK ? s : pd_time_fft_inv(c, pd_spec_local(c->Sh, c->S), u, c->S, acc);
 }
 
 pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {

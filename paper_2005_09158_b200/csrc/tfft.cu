@@ -29,9 +29,9 @@ struct TileCfg {
 // ---------------------------------------------------------------------------------------------
 // Step (a): r (real) -> Gamma r -> FFT over time -> half spectrum.
 // ---------------------------------------------------------------------------------------------
-template <int N>
+template <int N, bool SH>
 __global__ void __launch_bounds__(TileCfg<N>::NTH, TileCfg<N>::MINB)
-tfft_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long long S,
+tfft_fwd_kernel(const double* __restrict__ r, const pd_spec sp, long long S,
                 const double* __restrict__ gam, const double2* __restrict__ tw) {
   using T = TileCfg<N>;
   constexpr int C = T::C, NTH = T::NTH;
@@ -74,7 +74,6 @@ tfft_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long lon
   __syncthreads();
   // separate the two real columns: X_n = (Z_n + conj Z_{N-n})/2, Y_n = -i (Z_n - conj Z_{N-n})/2
   constexpr int NOUT = (N / 2 + 1) * 2 * C;
-  double2* out = Sh + s0;
 #pragma unroll 4
   for (int o = threadIdx.x; o < NOUT; o += NTH) {
     const int col = o % (2 * C), n = o / (2 * C), c = col >> 1;
@@ -85,7 +84,7 @@ tfft_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long lon
       v = make_double2(0.5 * (z1.y + z2.y), -0.5 * (z1.x - z2.x));
     else
       v = make_double2(0.5 * (z1.x + z2.x), 0.5 * (z1.y - z2.y));
-    if (full || s0 + col < S) __stcs(out + (long long)n * S + col, v);
+    if (full || s0 + col < S) __stcs(pd_spec_row<SH>(sp, n) + s0 + col, v);
   }
 }
 
@@ -93,9 +92,9 @@ tfft_fwd_kernel(const double* __restrict__ r, double2* __restrict__ Sh, long lon
 // Step (c): half spectrum -> inverse FFT over time -> Gamma^{-1}/Nt -> real.
 // MODE 0: z = result.  MODE 1: z += result (fused stationary update u <- u + P^{-1} r).
 // ---------------------------------------------------------------------------------------------
-template <int N, int MODE>
+template <int N, int MODE, bool SH>
 __global__ void __launch_bounds__(TileCfg<N>::NTH, TileCfg<N>::MINB)
-tfft_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long long S,
+tfft_inv_kernel(const pd_spec sp, double* __restrict__ z, long long S,
                 const double* __restrict__ igam, const double2* __restrict__ tw) {
   using T = TileCfg<N>;
   constexpr int C = T::C, NTH = T::NTH;
@@ -114,7 +113,6 @@ tfft_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long lon
   }
   // stage the half-spectrum tile H[n][col], n = 0..N/2, col = 0..2C-1 (coalesced rows)
   constexpr int NIN = (N / 2 + 1) * 2 * C;
-  const double2* in = Sh + s0;
   {
     // all of a thread's loads in flight before the first smem store
     constexpr int PT = (NIN + NTH - 1) / NTH;
@@ -123,7 +121,7 @@ tfft_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long lon
     for (int k = 0; k < PT; ++k) {
       const int o = threadIdx.x + k * NTH;
       const int col = o % (2 * C), n = o / (2 * C);
-      v[k] = (o < NIN && (full || s0 + col < S)) ? __ldcs(in + (long long)n * S + col) : czero();
+      v[k] = (o < NIN && (full || s0 + col < S)) ? __ldcs(pd_spec_row<SH>(sp, n) + s0 + col) : czero();
     }
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
@@ -173,7 +171,7 @@ tfft_inv_kernel(const double2* __restrict__ Sh, double* __restrict__ z, long lon
 }
 
 template <int N>
-cudaError_t launch_fwd_n(const double* r, double2* Sh, long long S, const double* gam, const double2* tw,
+cudaError_t launch_fwd_n(const double* r, const pd_spec& sp, long long S, const double* gam, const double2* tw,
                          cudaStream_t st) {
   using T = TileCfg<N>;
   const int smem = smem_elems(N * T::C) * (int)sizeof(double2);
@@ -181,17 +179,22 @@ cudaError_t launch_fwd_n(const double* r, double2* Sh, long long S, const double
   int dev_ = 0;
   cudaGetDevice(&dev_);
   if (attr != dev_) {
-    cudaError_t e = cudaFuncSetAttribute(tfft_fwd_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(tfft_fwd_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tfft_fwd_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = dev_;
   }
   const long long tiles = (S + 2 * T::C - 1) / (2 * T::C);
-  tfft_fwd_kernel<N><<<(unsigned)tiles, T::NTH, smem, st>>>(r, Sh, S, gam, tw);
+  if (sp.P > 1)
+    tfft_fwd_kernel<N, true><<<(unsigned)tiles, T::NTH, smem, st>>>(r, sp, S, gam, tw);
+  else
+    tfft_fwd_kernel<N, false><<<(unsigned)tiles, T::NTH, smem, st>>>(r, sp, S, gam, tw);
   return cudaGetLastError();
 }
 
 template <int N>
-cudaError_t launch_inv_n(const double2* Sh, double* z, long long S, const double* igam, const double2* tw,
+cudaError_t launch_inv_n(const pd_spec& sp, double* z, long long S, const double* igam, const double2* tw,
                          int accumulate, cudaStream_t st) {
   using T = TileCfg<N>;
   const int smem = smem_elems((N / 2 + 1) * 2 * T::C) * (int)sizeof(double2);
@@ -199,17 +202,26 @@ cudaError_t launch_inv_n(const double2* Sh, double* z, long long S, const double
   int dev_ = 0;
   cudaGetDevice(&dev_);
   if (attr != dev_) {
-    cudaError_t e = cudaFuncSetAttribute(tfft_inv_kernel<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(tfft_inv_kernel<N, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(tfft_inv_kernel<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e = cudaFuncSetAttribute(tfft_inv_kernel<N, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tfft_inv_kernel<N, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tfft_inv_kernel<N, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = dev_;
   }
   const long long tiles = (S + 2 * T::C - 1) / (2 * T::C);
-  if (accumulate)
-    tfft_inv_kernel<N, 1><<<(unsigned)tiles, T::NTH, smem, st>>>(Sh, z, S, igam, tw);
+  const bool sh = sp.P > 1;
+  if (accumulate && sh)
+    tfft_inv_kernel<N, 1, true><<<(unsigned)tiles, T::NTH, smem, st>>>(sp, z, S, igam, tw);
+  else if (accumulate)
+    tfft_inv_kernel<N, 1, false><<<(unsigned)tiles, T::NTH, smem, st>>>(sp, z, S, igam, tw);
+  else if (sh)
+    tfft_inv_kernel<N, 0, true><<<(unsigned)tiles, T::NTH, smem, st>>>(sp, z, S, igam, tw);
   else
-    tfft_inv_kernel<N, 0><<<(unsigned)tiles, T::NTH, smem, st>>>(Sh, z, S, igam, tw);
+    tfft_inv_kernel<N, 0, false><<<(unsigned)tiles, T::NTH, smem, st>>>(sp, z, S, igam, tw);
   return cudaGetLastError();
 }
 
@@ -229,16 +241,16 @@ unsigned blocks1(long long S) { return (unsigned)std::min<long long>((S + 255) /
 
 int pd_tfft_supported(int nt) { return nt >= 1 && nt <= 8192 && (nt & (nt - 1)) == 0; }
 
-cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+cudaError_t pd_launch_tfft_fwd(int nt, const double* r, const pd_spec& sp, long long S, const double* gam,
                                const double2* tw, cudaStream_t st) {
   if (nt == 1) {
-    tfft1_fwd_kernel<<<blocks1(S), 256, 0, st>>>(r, Sh, S);
+    tfft1_fwd_kernel<<<blocks1(S), 256, 0, st>>>(r, pd_spec_row(sp, 0), S);
     return cudaGetLastError();
   }
   switch (nt) {
 #define PD_CASE(n) \
   case n:          \
-    return launch_fwd_n<n>(r, Sh, S, gam, tw, st);
+    return launch_fwd_n<n>(r, sp, S, gam, tw, st);
     PD_CASE(2) PD_CASE(4) PD_CASE(8) PD_CASE(16) PD_CASE(32) PD_CASE(64) PD_CASE(128) PD_CASE(256)
     PD_CASE(512) PD_CASE(1024) PD_CASE(2048) PD_CASE(4096) PD_CASE(8192)
 #undef PD_CASE
@@ -247,16 +259,16 @@ cudaError_t pd_launch_tfft_fwd(int nt, const double* r, double2* Sh, long long S
   }
 }
 
-cudaError_t pd_launch_tfft_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+cudaError_t pd_launch_tfft_inv(int nt, const pd_spec& sp, double* z, long long S, const double* igam,
                                const double2* tw, int accumulate, cudaStream_t st) {
   if (nt == 1) {
-    tfft1_inv_kernel<<<blocks1(S), 256, 0, st>>>(Sh, z, S, accumulate);
+    tfft1_inv_kernel<<<blocks1(S), 256, 0, st>>>(pd_spec_row(sp, 0), z, S, accumulate);
     return cudaGetLastError();
   }
   switch (nt) {
 #define PD_CASE(n) \
   case n:          \
-    return launch_inv_n<n>(Sh, z, S, igam, tw, accumulate, st);
+    return launch_inv_n<n>(sp, z, S, igam, tw, accumulate, st);
     PD_CASE(2) PD_CASE(4) PD_CASE(8) PD_CASE(16) PD_CASE(32) PD_CASE(64) PD_CASE(128) PD_CASE(256)
     PD_CASE(512) PD_CASE(1024) PD_CASE(2048) PD_CASE(4096) PD_CASE(8192)
 #undef PD_CASE

@@ -38,10 +38,10 @@ struct Cfg2 {  // stage FFT of length N over C sequences
 // t1 of Y[t1][n2][.], then separation of the two real columns on the half spectrum rows n <= Nt/2.
 // Sequences c in [0, 2P): c < P -> residue n2, pair c;  c >= P -> residue n2' = (N2-n2)%N2, pair c-P.
 // ---------------------------------------------------------------------------------------------
-template <int NT, int RM = 16>
+template <int NT, int RM = 16, bool SH = false>
 __global__ void __launch_bounds__(2 * kP * (NT / kN2) / elems_per_thread(NT / kN2, RM))
 tf4_fwd_s2(const double2* __restrict__ Y, long long S, long long p_begin, long long npairs_chunk,
-           double2* __restrict__ Sh, const double2* __restrict__ tw1) {
+           const pd_spec sp, const double2* __restrict__ tw1) {
   constexpr int N1 = NT / kN2, C = 2 * kP, NTH = C * N1 / elems_per_thread(N1, RM);
   extern __shared__ double2 sm[];
   __shared__ double2 s_tw1[N1];
@@ -93,7 +93,7 @@ tf4_fwd_s2(const double2* __restrict__ Y, long long S, long long p_begin, long l
     else
       v = make_double2(0.5 * (z1.x + z2.x), 0.5 * (z1.y - z2.y));
     const long long gcol = 2 * p0 + col;
-    if (pl0 + pc < Pc && gcol < S) __stcs(Sh + (long long)n * S + gcol, v);
+    if (pl0 + pc < Pc && gcol < S) __stcs(pd_spec_row<SH>(sp, n) + gcol, v);
   }
 }
 
@@ -101,9 +101,9 @@ tf4_fwd_s2(const double2* __restrict__ Y, long long S, long long p_begin, long l
 // inverse stage 1: for residues (n2, N2-n2): rebuild Z[n] = X[n] + i Y[n] from the half spectrum, N1-point
 // inverse FFTs over n1, times w_Nt^{-t1 n2}; writes W[n2][t1][pl].
 // ---------------------------------------------------------------------------------------------
-template <int NT, int RM = 16>
+template <int NT, int RM = 16, bool SH = false>
 __global__ void __launch_bounds__(2 * kP * (NT / kN2) / elems_per_thread(NT / kN2, RM))
-tf4_inv_s1(const double2* __restrict__ Sh, long long S, long long p_begin, long long npairs_chunk,
+tf4_inv_s1(const pd_spec sp, long long S, long long p_begin, long long npairs_chunk,
            double2* __restrict__ W, const double2* __restrict__ tw1, const double2* __restrict__ twt) {
   constexpr int N1 = NT / kN2, C = 2 * kP, NTH = C * N1 / elems_per_thread(N1, RM);
   extern __shared__ double2 sm[];
@@ -133,7 +133,7 @@ tf4_inv_s1(const double2* __restrict__ Sh, long long S, long long p_begin, long 
       const int n = (set == 0 ? n2 : n2p) + kN2 * n1;
       const long long gcol = 2 * p0 + col;
       v[k] = czero();
-      if (o < total && n <= NT / 2 && pl0 + (col >> 1) < Pc && gcol < S) v[k] = __ldcs(Sh + (long long)n * S + gcol);
+      if (o < total && n <= NT / 2 && pl0 + (col >> 1) < Pc && gcol < S) v[k] = __ldcs(pd_spec_row<SH>(sp, n) + gcol);
     }
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
@@ -176,7 +176,7 @@ tf4_inv_s1(const double2* __restrict__ Sh, long long S, long long p_begin, long 
 
 // non-persistent grid versions: one CTA per tile
 template <int NT, int RM>
-void fwd_grid(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
+void fwd_grid(const double* r, const pd_spec& sp, long long S, const double* gam, const pd_tf4_tables& tb,
               double2* scratch, long long p, long long pc, bool vec, cudaStream_t st) {
   constexpr int N1 = NT / kN2;
   const int sm1 = smem_of<kN2>(kP), sm2 = smem_of<N1>(2 * kP);
@@ -186,7 +186,8 @@ void fwd_grid(const double* r, double2* Sh, long long S, const double* gam, cons
   if (attr != dev_) {
     cudaFuncSetAttribute(tf4_fwd_s1<NT, kN2, kP, true, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(tf4_fwd_s1<NT, kN2, kP, false, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
-    cudaFuncSetAttribute(tf4_fwd_s2<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_fwd_s2<NT, RM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(tf4_fwd_s2<NT, RM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     attr = dev_;
   }
   const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
@@ -195,11 +196,14 @@ void fwd_grid(const double* r, double2* Sh, long long S, const double* gam, cons
     tf4_fwd_s1<NT, kN2, kP, true, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
   else
     tf4_fwd_s1<NT, kN2, kP, false, RM><<<g1, kP * kN2 / RM, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
-  tf4_fwd_s2<NT, RM><<<g2, 2 * kP * N1 / elems_per_thread(N1, RM), sm2, st>>>(scratch, S, p, pc, Sh, tb.tw1);
+  if (sp.P > 1)
+    tf4_fwd_s2<NT, RM, true><<<g2, 2 * kP * N1 / elems_per_thread(N1, RM), sm2, st>>>(scratch, S, p, pc, sp, tb.tw1);
+  else
+    tf4_fwd_s2<NT, RM, false><<<g2, 2 * kP * N1 / elems_per_thread(N1, RM), sm2, st>>>(scratch, S, p, pc, sp, tb.tw1);
 }
 
 template <int NT, int RM>
-void inv_grid(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
+void inv_grid(const pd_spec& sp, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
               double2* scratch, long long p, long long pc, int accumulate, bool vec, cudaStream_t st) {
   constexpr int N1 = NT / kN2;
   const int sm1 = smem_of<N1>(2 * kP) > smem_elems(2 * N1 * 2 * kP) * (int)sizeof(double2)
@@ -210,7 +214,8 @@ void inv_grid(const double2* Sh, double* z, long long S, const double* igam, con
   int dev_ = 0;
   cudaGetDevice(&dev_);
   if (attr != dev_) {
-    cudaFuncSetAttribute(tf4_inv_s1<NT, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_inv_s1<NT, RM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(tf4_inv_s1<NT, RM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, true, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, true, 1, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(tf4_inv_s2<NT, kN2, kP, false, 0, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -219,7 +224,10 @@ void inv_grid(const double2* Sh, double* z, long long S, const double* igam, con
   }
   const unsigned nt1 = (unsigned)((pc + kP - 1) / kP);
   const dim3 g1(nt1, kN2 / 2 + 1), g2(nt1, N1);
-  tf4_inv_s1<NT, RM><<<g1, 2 * kP * N1 / elems_per_thread(N1, RM), sm1, st>>>(Sh, S, p, pc, scratch, tb.tw1, tb.twt);
+  if (sp.P > 1)
+    tf4_inv_s1<NT, RM, true><<<g1, 2 * kP * N1 / elems_per_thread(N1, RM), sm1, st>>>(sp, S, p, pc, scratch, tb.tw1, tb.twt);
+  else
+    tf4_inv_s1<NT, RM, false><<<g1, 2 * kP * N1 / elems_per_thread(N1, RM), sm1, st>>>(sp, S, p, pc, scratch, tb.tw1, tb.twt);
   const int th2 = kP * kN2 / RM;
   if (vec) {
     if (accumulate)
@@ -238,7 +246,7 @@ constexpr int kRmaxGrid = 8;  // radix-8 passes: 8 elements per thread, twice th
 
 // chunk ci of a call: stream / scratch ci mod K of the optional pipeline (kernels.h pd_tfx_overlap)
 template <int NT>
-cudaError_t fwd_n(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
+cudaError_t fwd_n(const double* r, const pd_spec& sp, long long S, const double* gam, const pd_tf4_tables& tb,
                   double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl, const pd_tfx_overlap* ov) {
   const bool vec = (S % 2 == 0) && ((reinterpret_cast<uintptr_t>(r) & 15) == 0);
   const long long npairs = (S + 1) / 2;
@@ -247,7 +255,7 @@ cudaError_t fwd_n(const double* r, double2* Sh, long long S, const double* gam, 
   for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
     const int lane = ov ? (int)(ci % ov->k) : 0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
-    fwd_grid<NT, kRmaxGrid>(r, Sh, S, gam, tb, lane ? ov->scratch[lane] : scratch0, p, pc, vec,
+    fwd_grid<NT, kRmaxGrid>(r, sp, S, gam, tb, lane ? ov->scratch[lane] : scratch0, p, pc, vec,
                             lane ? ov->st[lane] : st0);
     n += 2;
   }
@@ -256,7 +264,7 @@ cudaError_t fwd_n(const double* r, double2* Sh, long long S, const double* gam, 
 }
 
 template <int NT>
-cudaError_t inv_n(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
+cudaError_t inv_n(const pd_spec& sp, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
                   double2* scratch0, long long chunk_pairs, int accumulate, cudaStream_t st0, int* nl,
                   const pd_tfx_overlap* ov) {
   const bool vec = (S % 2 == 0) && ((reinterpret_cast<uintptr_t>(z) & 15) == 0);
@@ -266,7 +274,7 @@ cudaError_t inv_n(const double2* Sh, double* z, long long S, const double* igam,
   for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
     const int lane = ov ? (int)(ci % ov->k) : 0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
-    inv_grid<NT, kRmaxGrid>(Sh, z, S, igam, tb, lane ? ov->scratch[lane] : scratch0, p, pc, accumulate, vec,
+    inv_grid<NT, kRmaxGrid>(sp, z, S, igam, tb, lane ? ov->scratch[lane] : scratch0, p, pc, accumulate, vec,
                             lane ? ov->st[lane] : st0);
     n += 2;
   }
@@ -280,26 +288,26 @@ int pd_tf4_supported(int nt) { return nt == 1024 || nt == 2048 || nt == 4096; }
 int pd_tf4_n2() { return kN2; }
 int pd_tf4_pairs_per_tile() { return kP; }
 
-cudaError_t pd_launch_tf4_fwd(int nt, const double* r, double2* Sh, long long S, const double* gam,
+cudaError_t pd_launch_tf4_fwd(int nt, const double* r, const pd_spec& sp, long long S, const double* gam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, cudaStream_t st,
                               int* nl, const pd_tfx_overlap* ov) {
   switch (nt) {
-    case 1024: return fwd_n<1024>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
-    case 2048: return fwd_n<2048>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
-    case 4096: return fwd_n<4096>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
-    case 8192: return fwd_n<8192>(r, Sh, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 1024: return fwd_n<1024>(r, sp, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 2048: return fwd_n<2048>(r, sp, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 4096: return fwd_n<4096>(r, sp, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
+    case 8192: return fwd_n<8192>(r, sp, S, gam, tb, scratch, chunk_pairs, st, nl, ov);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t pd_launch_tf4_inv(int nt, const double2* Sh, double* z, long long S, const double* igam,
+cudaError_t pd_launch_tf4_inv(int nt, const pd_spec& sp, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, double2* scratch, long long chunk_pairs, int accumulate,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov) {
   switch (nt) {
-    case 1024: return inv_n<1024>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
-    case 2048: return inv_n<2048>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
-    case 4096: return inv_n<4096>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
-    case 8192: return inv_n<8192>(Sh, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 1024: return inv_n<1024>(sp, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 2048: return inv_n<2048>(sp, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 4096: return inv_n<4096>(sp, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
+    case 8192: return inv_n<8192>(sp, z, S, igam, tb, scratch, chunk_pairs, accumulate, st, nl, ov);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -55,8 +55,12 @@ constexpr int kRX = PD_TFX_RM;
 #define PD_TFX_XFIRST_INV PD_TFX_XFIRST
 #endif
 #ifndef PD_TFX_KPT
-#define PD_TFX_KPT 4096  // elements of a stage-1 tile (N2 x KP pairs)
+#define PD_TFX_KPT 4096  // elements of a stage-1 tile (N2 x KP pairs), Nt >= 1024
 #endif
+#ifndef PD_TFX_KPT_SMALL
+#define PD_TFX_KPT_SMALL 2048  // Nt <= 512 (cfg3: 0.091 / 0.085 ms fwd / inv vs 0.095 / 0.092 with 4096, r02g)
+#endif
+__host__ __device__ constexpr int tfx_kpt(int nt) { return nt <= 512 ? PD_TFX_KPT_SMALL : PD_TFX_KPT; }
 constexpr int kRS = PD_TFX_S1_RM;
 
 template <int NT, int NX>
@@ -64,16 +68,16 @@ struct Fx {
   static constexpr int N1 = kN1, N2 = NT / kN1, NP = NX / 2, C = 2 * NP, NTH = 8 * NX / kRX;
   static constexpr int ROWS = 2 * N1;                 // rows (n1, set) of NP values
   static constexpr int SMEM = smem_elems(ROWS * NP);  // complex elements
-  static constexpr int KP = PD_TFX_KPT / N2 < 8 ? 8 : PD_TFX_KPT / N2;  // stage-1 pairs per tile (N2 * KP = KPT)
+  static constexpr int KP = tfx_kpt(NT) / N2 < 8 ? 8 : tfx_kpt(NT) / N2;  // stage-1 pairs per tile (N2 * KP = KPT)
 };
 
 // ---------------------------------------------------------------------------------------------
 // forward stage 2 + x-FFT
 // ---------------------------------------------------------------------------------------------
-template <int NT, int NX>
+template <int NT, int NX, bool SH>
 __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2(const double2* __restrict__ Y, long long S,
                                                              long long p_begin, long long Pc,
-                                                             double2* __restrict__ Sh,
+                                                             const pd_spec sp,
                                                              const double2* __restrict__ twx) {
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, C = F::C, NTH = F::NTH;
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2(const
     const int m = (NT - n) & (NT - 1);
     const int setp = (m % N2) == n2 ? 0 : 1, n1p = m / N2;
     const int ra = (2 * n1 + set) * NP, rb = (2 * n1p + setp) * NP;
-    double2* out = Sh + (long long)n * S + 2 * p0;
+    double2* out = pd_spec_row<SH>(sp, n) + 2 * p0;
 #pragma unroll
     for (int kx = threadIdx.x; kx < NX; kx += NTH) {
       const int k = kx & (NP - 1);
@@ -142,8 +146,8 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2(const
 // ---------------------------------------------------------------------------------------------
 // x-IFFT + inverse stage 1
 // ---------------------------------------------------------------------------------------------
-template <int NT, int NX>
-__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1(const double2* __restrict__ Sh, long long S,
+template <int NT, int NX, bool SH>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1(const pd_spec sp, long long S,
                                                              long long p_begin, long long Pc,
                                                              double2* __restrict__ W,
                                                              const double2* __restrict__ twx,
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1(const
       const int set = r / N1, n1 = r % N1;
       const int n = (set ? n2p : n2) + N2 * n1;
       if (set < nsets && n <= NT / 2) {
-        const double2* q = Sh + (long long)n * S + 2 * p0 + k;
+        const double2* q = pd_spec_row<SH>(sp, n) + 2 * p0 + k;
         x0[r] = __ldcs(q);
         x1[r] = __ldcs(q + NP);
       }
@@ -250,10 +254,10 @@ PD_D void untangle_store(double2* out, int i, double2 x, double2 y, double2 w) {
   __stcs(out + i + NP, csub(E, wO));
 }
 
-template <int NT, int NX>
+template <int NT, int NX, bool SH>
 __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(const double2* __restrict__ Y, long long S,
                                                               long long p_begin, long long Pc,
-                                                              double2* __restrict__ Sh,
+                                                              const pd_spec sp,
                                                               const double2* __restrict__ twx) {
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
@@ -302,14 +306,14 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(cons
       const int n = n2 + N2 * n1;
       if (n <= NT / 2) {
         const double2 y = n2 == 0 ? b[(N1 - n1) & (N1 - 1)] : b[N1 - 1 - n1];
-        untangle_store<NP>(Sh + (long long)n * S + 2 * p0, k, a[n1], y, wk);
+        untangle_store<NP>(pd_spec_row<SH>(sp, n) + 2 * p0, k, a[n1], y, wk);
       }
     }
     if (nsets == 2) {
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const int n = n2p + N2 * n1;
-        if (n <= NT / 2) untangle_store<NP>(Sh + (long long)n * S + 2 * p0, kb, b[n1], a[N1 - 1 - n1], wb);
+        if (n <= NT / 2) untangle_store<NP>(pd_spec_row<SH>(sp, n) + 2 * p0, kb, b[n1], a[N1 - 1 - n1], wb);
       }
     }
   }
@@ -326,8 +330,8 @@ PD_D double2 a_mirror(double2 x0, double2 x1, double2 wi) {
   return make_double2(E.x + O.y, O.x - E.y);
 }
 
-template <int NT, int NX>
-__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(const double2* __restrict__ Sh, long long S,
+template <int NT, int NX, bool SH>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(const pd_spec sp, long long S,
                                                               long long p_begin, long long Pc,
                                                               double2* __restrict__ W,
                                                               const double2* __restrict__ twx,
@@ -355,12 +359,12 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(cons
     for (int n1 = 0; n1 < NV; ++n1) {
       const int na = n2 + N2 * n1, nb = rb + N2 * n1;
       if (na <= NT / 2) {
-        const double2* q = Sh + (long long)na * S + 2 * p0 + k;
+        const double2* q = pd_spec_row<SH>(sp, na) + 2 * p0 + k;
         x0[n1] = __ldcs(q);
         x1[n1] = __ldcs(q + NP);
       }
       if (nb <= NT / 2) {
-        const double2* q = Sh + (long long)nb * S + 2 * p0 + kb;
+        const double2* q = pd_spec_row<SH>(sp, nb) + 2 * p0 + kb;
         y0[n1] = __ldcs(q);
         y1[n1] = __ldcs(q + NP);
       }
@@ -429,10 +433,12 @@ void set_attrs() {
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, true, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, false, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_fwd_s1_comb<NT, N2, KP, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
-  cudaFuncSetAttribute(tfx_fwd_s2<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-  cudaFuncSetAttribute(tfx_inv_s1<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-  cudaFuncSetAttribute(tfx_fwd_s2x<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-  cudaFuncSetAttribute(tfx_inv_s1x<NT, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_fwd_s2<NT, NX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_inv_s1<NT, NX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_fwd_s2x<NT, NX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_inv_s1x<NT, NX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_fwd_s2x<NT, NX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  cudaFuncSetAttribute(tfx_inv_s1x<NT, NX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, true, 1, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_inv_s2<NT, N2, KP, false, 0, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
@@ -441,7 +447,7 @@ void set_attrs() {
 }
 
 template <int NT, int NX>
-cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, const pd_tf4_tables& tb,
+cudaError_t fwd(const double* r, const pd_spec& sp, long long S, const double* gam, const pd_tf4_tables& tb,
                 const double2* twx, double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl,
                 const pd_tfx_overlap* ov, const pd_comb_args* comb) {
   using F = Fx<NT, NX>;
@@ -467,10 +473,14 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
       tf4_fwd_s1<NT, N2, KP, true, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
     else
       tf4_fwd_s1<NT, N2, KP, false, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
-    if (PD_TFX_XFIRST_FWD)
-      tfx_fwd_s2x<NT, NX><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, Sh, twx);
+    if (PD_TFX_XFIRST_FWD && sp.P > 1)
+      tfx_fwd_s2x<NT, NX, true><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, sp, twx);
+    else if (PD_TFX_XFIRST_FWD)
+      tfx_fwd_s2x<NT, NX, false><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, sp, twx);
+    else if (sp.P > 1)
+      return cudaErrorInvalidValue;  // the t1-first A/B kernels (PD_TFX_XFIRST=0) are single-GPU only
     else
-      tfx_fwd_s2<NT, NX><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, Sh, twx);
+      tfx_fwd_s2<NT, NX, false><<<g2, F::NTH, sm2, st>>>(scratch, S, p, pc, sp, twx);
     n += 2;
   }
   *nl = n;
@@ -478,7 +488,7 @@ cudaError_t fwd(const double* r, double2* Sh, long long S, const double* gam, co
 }
 
 template <int NT, int NX>
-cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
+cudaError_t inv(const pd_spec& sp, double* z, long long S, const double* igam, const pd_tf4_tables& tb,
                 const double2* twx, double2* scratch0, long long chunk_pairs, int accumulate, cudaStream_t st0,
                 int* nl, const pd_tfx_overlap* ov) {
   using F = Fx<NT, NX>;
@@ -495,10 +505,14 @@ cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, c
     double2* scratch = lane ? ov->scratch[lane] : scratch0;
     const long long pc = npairs - p < chunk_pairs ? npairs - p : chunk_pairs;
     const dim3 g1((unsigned)(pc / NP), N2 / 2 + 1), g2((unsigned)((pc + KP - 1) / KP), kN1);
-    if (PD_TFX_XFIRST_INV)
-      tfx_inv_s1x<NT, NX><<<g1, F::NTH, sm2, st>>>(Sh, S, p, pc, scratch, twx, tb.twt);
+    if (PD_TFX_XFIRST_INV && sp.P > 1)
+      tfx_inv_s1x<NT, NX, true><<<g1, F::NTH, sm2, st>>>(sp, S, p, pc, scratch, twx, tb.twt);
+    else if (PD_TFX_XFIRST_INV)
+      tfx_inv_s1x<NT, NX, false><<<g1, F::NTH, sm2, st>>>(sp, S, p, pc, scratch, twx, tb.twt);
+    else if (sp.P > 1)
+      return cudaErrorInvalidValue;
     else
-      tfx_inv_s1<NT, NX><<<g1, F::NTH, sm2, st>>>(Sh, S, p, pc, scratch, twx, tb.twt);
+      tfx_inv_s1<NT, NX, false><<<g1, F::NTH, sm2, st>>>(sp, S, p, pc, scratch, twx, tb.twt);
     const int th = KP * N2 / kRS;
     if (vec) {
       if (accumulate)
@@ -521,7 +535,7 @@ cudaError_t inv(const double2* Sh, double* z, long long S, const double* igam, c
 
 // Nt = 256 / 512 too since r02: with the y-pass by cyclic Toeplitz solves the fold wins at cfg3 (apply 0.283 ->
 // 0.230 ms: the slab x-FFT row passes leave Step (b)); PD_TFX_SMALL=0 restores the single-tile FFT + row passes.
-// NX = 1024 (instantiated, not parity-tested: Nt >= 1024 makes it 1e9 dofs) takes the tf4 + slab route.
+// NX = 1024 (Nt >= 256 makes it >= 2.7e8 dofs per real vector) takes the single-tile / tf4 + slab route.
 int pd_tfx_supported(int nt, int nx) {
   const char* se = getenv("PD_TFX_SMALL");
   const bool small = se == nullptr || atoi(se) != 0;
@@ -531,7 +545,7 @@ int pd_tfx_supported(int nt, int nx) {
 }
 int pd_tfx_n2(int nt) { return nt / kN1; }
 long long pd_tfx_chunk_align(int nt, int nx) {
-  const long long kp = PD_TFX_KPT / (nt / kN1) < 8 ? 8 : PD_TFX_KPT / (nt / kN1);
+  const long long kp = tfx_kpt(nt) / (nt / kN1) < 8 ? 8 : tfx_kpt(nt) / (nt / kN1);
   const long long np = nx / 2;
   return kp > np ? kp : np;
 }
@@ -541,8 +555,7 @@ long long pd_tfx_chunk_align(int nt, int nx) {
   case T * 10000 + 64: return FN<T, 64> ARGS;                                                       \
   case T * 10000 + 128: return FN<T, 128> ARGS;                                                     \
   case T * 10000 + 256: return FN<T, 256> ARGS;                                                     \
-  case T * 10000 + 512: return FN<T, 512> ARGS;                                                     \
-  case T * 10000 + 1024: return FN<T, 1024> ARGS;
+  case T * 10000 + 512: return FN<T, 512> ARGS;
 #define PD_TFX_SWITCH(FN, ARGS)                                                                      \
   switch (nt * 10000 + nx) {                                                                         \
     PD_TFX_ROW(256, FN, ARGS) PD_TFX_ROW(512, FN, ARGS)                                              \
@@ -550,14 +563,14 @@ long long pd_tfx_chunk_align(int nt, int nx) {
     default: return cudaErrorInvalidValue;                                                           \
   }
 
-cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, double2* Sh, long long S, const double* gam,
+cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, const pd_spec& sp, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov, const pd_comb_args* comb) {
-  PD_TFX_SWITCH(fwd, (r, Sh, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov, comb))
+  PD_TFX_SWITCH(fwd, (r, sp, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov, comb))
 }
 
-cudaError_t pd_launch_tfx_inv(int nt, int nx, const double2* Sh, double* z, long long S, const double* igam,
+cudaError_t pd_launch_tfx_inv(int nt, int nx, const pd_spec& sp, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               int accumulate, cudaStream_t st, int* nl, const pd_tfx_overlap* ov) {
-  PD_TFX_SWITCH(inv, (Sh, z, S, igam, tb, twx, scratch, chunk_pairs, accumulate, st, nl, ov))
+  PD_TFX_SWITCH(inv, (sp, z, S, igam, tb, twx, scratch, chunk_pairs, accumulate, st, nl, ov))
 }
