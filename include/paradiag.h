@@ -159,9 +159,10 @@ PD_API pd_status pd_solve(pd_ctx* ctx, int solver, const double* b, double* u, d
  * residual-form solvers above; per iteration the work is the tail map below plus O(H S) vector operations
  * instead of full passes over Nt x S.  Sharded contexts (NCCL or virtual ranks) replicate the H head / tail blocks
  * on every rank: the 1D tail map splits its frequencies over the ranks and all-reduces the H x S tail, the 2D one
- * runs replicated (tailform.cpp).  PD_EINVAL when Nt < 2H and for PD_WAVE2D_DIRICHLET (no tail map).  Per-context
- * tables (1D: F x H coefficients; 2D: the N x N transfer function tau, F N^2 divisions) are built on the first call
- * and kept.
+ * runs replicated (tailform.cpp).  PD_EINVAL when Nt < 2H, and for 1D contexts whose Step (b) uses the pivoted
+ * fallback (the tail map needs the recurrence solver).  Per-context tables (1D: F x H coefficients; 2D periodic: the
+ * N x N transfer function tau, F N^2 divisions; 2D Dirichlet: H x H real transfer tables in the DST-I basis and the
+ * N x N sine table, the map then being two dense 2D DSTs per head block) are built on the first call and kept.
  *
  * pd_tail_map: tail = last H blocks of P_alpha^{-1} (E_H head), head and tail device [H][local dofs]
  *   (must not alias).  Economical Step (a), Step (b) for every frequency, last H rows of Step (c). */

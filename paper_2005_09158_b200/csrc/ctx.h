@@ -89,6 +89,8 @@ struct pd_ctx {
   int* gtsv_bad = nullptr;       // device: max (frequency + 1) with a zero / non-finite pivot (0: none)
   int* gtsv_hbad = nullptr;      // pinned host copy
   double* mu = nullptr;          // 2D Dirichlet: [M] DST eigenvalues (4 nu/h^2) sin^2(pi k / M), M = 2(N+1)
+  pd_dtri_coef* dtri = nullptr;  // 2D Dirichlet: [F][N] y-direction recurrence constants (slab2d.cu dtri)
+  bool use_dtri = false;
   bool use_ytri = false;
   pd_slab_params slab{};
   int slab_chunk = 1;
@@ -139,6 +141,9 @@ struct pd_ctx {
     pd_stencil gsten{};       // stencil of the GLOBAL grid (heads and tails are replicated on every rank)
     double2* tau = nullptr;   // 2D: [N][N] transfer function
     double2* work = nullptr;  // 2D: [N][N] complex slab
+    double* taud = nullptr;   // 2D Dirichlet: [H][H][N][N] real transfer tables
+    double* dsin = nullptr;   // 2D Dirichlet: [N][N] DST-I sine table
+    double* dwork = nullptr;  // 2D Dirichlet: [2H + 1][N][N] transform work
     std::vector<double*> scr;  // head-sized scratch vectors
     std::vector<double*> Vh;   // reduced GMRES basis (heads)
     int* flag = nullptr;       // device flag (any non-zero)

@@ -155,6 +155,14 @@ int pd_slab2d_ytri_supported(int n);
 // 2D homogeneous Dirichlet (PD_WAVE2D_DIRICHLET): N = 2^k - 1 interior nodes; tensor DST-I via FFTs of length
 // M = 2(N+1) of the odd extension; mu[k] = (4 nu/h^2) sin^2(pi k/M), k < M; tw: M-point twiddles
 int pd_slab2d_dst_supported(int n);
+// 2D Dirichlet Step (b) as x-DST rows -> y Dirichlet Toeplitz solves per (n, kx) -> inverse x-DST rows (slab2d.cu
+// dtri): one table entry per (frequency, kx < N), the constants of pd_tri_coef plus g = 1/(1 - c q_0)
+struct pd_dtri_coef {
+  double2 r2, s, tau, c, r2L, sL, g;
+};
+int pd_slab2d_dtri_supported(int n);
+cudaError_t pd_launch_slab2d_dtri(double2* Sh, int n, int nfreq, int f0_glob, const pd_dtri_coef* coef,
+                                  const double2* tw, int chunk, cudaStream_t st, int* launches);
 // out[n] = min over (kx, ky) of |lam1_n + lam2_n kappa| / (|lam1_n| + |lam2_n| |kappa|)  (setup singularity check)
 cudaError_t pd_launch_min_den(const double2* lam1, const double2* lam2, const double* sx, const double* sn,
                               pd_slab_params prm, int n, int nfreq, double* out, cudaStream_t st);
@@ -221,6 +229,14 @@ cudaError_t pd_launch_head_G(const pd_stencil& p, const pd_tail_g& gc, const dou
 cudaError_t pd_launch_reduce_rows(const double* part, int G, long long len, double* out, cudaStream_t st);
 cudaError_t pd_launch_tau2d(double2* tau, int n, int nfreq, const double2* lam1, const double2* lam2, const double2* w,
                             const double* sx, const double* sn, pd_slab_params prm, cudaStream_t st);
+// 2D Dirichlet tail map (H blocks): tau[a][t][ky][kx] = Re sum_n w[a*H+t][n] / (lam1_n + lam2_n (mu[kx+1] + mu[ky+1]));
+// dense 2D DST-I Y = S X S of H real N x N blocks (S: N x N sine table, tmp: N x N); out_a = scale sum_t tau_at G_t
+cudaError_t pd_launch_tau_dir(double* tau, int n, int nfreq, int H, const double2* lam1, const double2* lam2,
+                              const double2* w, const double* mu, cudaStream_t st);
+cudaError_t pd_launch_dst2d_dense(const double* in, double* out, double* tmp, const double* S, int N, int H,
+                                  cudaStream_t st);
+cudaError_t pd_launch_tau_combine(const double* tau, const double* G, double* out, int N, int H, double scale,
+                                  cudaStream_t st);
 cudaError_t pd_launch_r2c(const double* g, double2* z, long long n, cudaStream_t st);
 cudaError_t pd_launch_take_real(const double2* z, double* out, long long n, cudaStream_t st);
 // Sh[n][x] = sum_{t<H} hc[n][t] gx[t][x] for n < F (Step (a) of a head-only vector)

@@ -215,6 +215,7 @@ static void free_ctx(pd_ctx* c) {
   if (!c) return;
   pd_tail_free(c);
   if (c->ytri) cudaFree(c->ytri);
+  if (c->dtri) cudaFree(c->dtri);
   if (c->mu) cudaFree(c->mu);
   if (c->nl_dbar) cudaFree(c->nl_dbar);
   if (c->gm_head) cudaFree(c->gm_head);
@@ -408,6 +409,63 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
     if (worst < 1e-13L) {
       free_ctx(c);
       return fail(nullptr, PD_ESINGULAR, "shifted system singular at frequency n=%d (relative |den| %.3Le)", wn, worst);
+    }
+    // y-direction by Dirichlet Toeplitz recurrences per (n, kx) (slab2d.cu dtri) when every column is in their
+    // stable regime; otherwise (or PD_NO_DTRI) the DST column pass
+    if (pd_slab2d_dtri_supported(N) && getenv("PD_NO_DTRI") == nullptr) {
+      const int L = (N + 1) / 32;
+      const long double a = -(long double)g->nu / ((long double)h * h), dia2 = 2 * (long double)g->nu / ((long double)h * h);
+      std::vector<pd_dtri_coef> dt((size_t)c->F * N);
+      bool ok = true;
+      auto cp = [](cld m, int e) {
+        cld r = 1.0L;
+        while (e) {
+          if (e & 1) r *= m;
+          m *= m;
+          e >>= 1;
+        }
+        return r;
+      };
+      for (int n = 0; n < c->F && ok; ++n)
+        for (int kx = 0; kx < N && ok; ++kx) {
+          const cld A = l2[n] * a, Cc = A, B = l1[n] + l2[n] * ((long double)hmu[kx + 1] + dia2);
+          const cld D = std::sqrt(B * B - 4.0L * A * Cc);
+          const cld den = std::abs(-B - D) >= std::abs(-B + D) ? -B - D : -B + D;
+          if (std::abs(den) == 0.0L) {
+            ok = false;
+            break;
+          }
+          const cld tau = 2.0L / den, r2 = A * tau, sv = Cc * tau;
+          if (!(powl(std::abs(r2), (long double)N) < 1e8L) || !(powl(std::abs(sv), (long double)N) < 1e8L)) {
+            ok = false;
+            break;
+          }
+          cld q0 = 0.0L, spw = 1.0L, rpw = r2;
+          for (int j = 0; j < N; ++j) {
+            q0 += spw * rpw;
+            spw *= sv;
+            rpw *= r2;
+          }
+          q0 *= -tau;
+          const cld piv = 1.0L - Cc * q0;
+          if (std::abs(piv) < 1e-12L) {
+            ok = false;
+            break;
+          }
+          pd_dtri_coef& t = dt[(size_t)n * N + kx];
+          t.r2 = d2(r2);
+          t.s = d2(sv);
+          t.tau = d2(tau);
+          t.c = d2(Cc);
+          t.r2L = d2(cp(r2, L));
+          t.sL = d2(cp(sv, L));
+          t.g = d2(1.0L / piv);
+        }
+      if (ok) {
+        SETUP_CUDA(dalloc(&c->dtri, dt.size()));
+        SETUP_CUDA(cudaMemcpy(c->dtri, dt.data(), dt.size() * sizeof(pd_dtri_coef), cudaMemcpyHostToDevice));
+        c->use_dtri = true;
+      }
     }
     std::vector<double2> htw = twiddles(M);
     SETUP_CUDA(dalloc(&c->mu, M));
@@ -667,8 +725,11 @@ pd_status pd_spatial_solve(pd_ctx* c, double2* Sh, int nfreq, int f0) {
   phase_begin(c, 1);
   if (c->g.op == PD_WAVE2D_DIRICHLET) {
     int nl = 0;
-    PD_CUDA(c, pd_launch_slab2d_dst(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->mu, c->tw_s, c->slab_chunk,
-                                    c->st, &nl));
+    if (c->use_dtri)
+      PD_CUDA(c, pd_launch_slab2d_dtri(Sh, c->g.nx, nfreq, f0, c->dtri, c->tw_s, c->slab_chunk, c->st, &nl));
+    else
+      PD_CUDA(c, pd_launch_slab2d_dst(Sh, c->g.nx, nfreq, c->lam1 + f0, c->lam2 + f0, c->mu, c->tw_s, c->slab_chunk,
+                                      c->st, &nl));
     c->launches += nl;
   } else if (c->g.op == PD_ADE2D_PERIODIC) {
     int nl = 0;

@@ -523,6 +523,137 @@ cudaError_t ytri_n(double2* Sh, int nfreq, int f0g, const pd_ytri_coef* coef, do
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// 2D Dirichlet Step (b) with the y-direction solved directly (T4A, PD_WAVE2D_DIRICHLET): after the x-DST row pass
+// every (frequency n, x-mode kx) column is the Dirichlet Toeplitz system
+//   a x_{y-1} + b x_y + a x_{y+1} = d_y,  x_{-1} = x_N = 0,  a = -lambda2 nu/h^2,  b = lambda1 + lambda2 (mu_kx + 2nu/h^2)
+// (K = -nu Lap_h = (mu_x) (x) I + I (x) T_y in the x-DST basis), solved by the characteristic-root recurrences of
+// tridiag.cu (forward w_i = r2 w_{i-1} + d_i, backward x_i = s x_{i+1} - tau w_i, rank-1 correction for x_0 with the
+// precomputed 1/(1 - c q_0)) on one warp per column, L = (N+1)/32 rows per lane (the last lane one row short), carries
+// by warp affine scans.  Replaces the column pass's length-2(N+1) FFT -> divide -> IFFT.  Scale 1/M of the x-DST
+// pair (forward and inverse odd-extension FFTs of length M = 2(N+1) multiply by M).
+template <int N1>
+__global__ void __launch_bounds__(32 * kYC, N1 <= 256 ? 3 : N1 <= 512 ? 2 : 1)
+dtri_kernel(double2* __restrict__ Sh, int slab0, int fglob0, const pd_dtri_coef* __restrict__ coef, double scale) {
+  constexpr int N = N1 - 1, L = N1 / 32, CS = N1 + 33;
+  extern __shared__ double2 sm[];
+  const int n = slab0 + blockIdx.y;
+  const int c0 = blockIdx.x * kYC;
+  double2* slab = Sh + (long long)n * N * N + c0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool colok = c0 + w < N;
+  const pd_dtri_coef cf = coef[(long long)(fglob0 + blockIdx.y) * N + (colok ? c0 + w : 0)];
+  {
+    constexpr int PT = L;  // ceil(N * kYC / (32 kYC)) = L
+    double2 v[PT];
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int i = threadIdx.x + k * 32 * kYC, r = i / kYC, c = i % kYC;
+      v[k] = (r < N && c0 + c < N) ? __ldcs(slab + (long long)r * N + c) : czero();
+    }
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int i = threadIdx.x + k * 32 * kYC, r = i / kYC, c = i % kYC;
+      sm[c * CS + r + r / L] = v[k];
+    }
+  }
+  __syncthreads();
+  double2* col = sm + w * CS + lane * (L + 1);
+  const int i0 = lane * L;
+  const int Lk = lane == 31 ? L - 1 : L;  // row N (= 32 L - 1) does not exist
+  double2 d[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) d[j] = j < Lk ? col[j] : czero();
+  // forward: w_i = r2 w_{i-1} + d_i, carry r2^L across lanes (lanes below 31 are full)
+  double2 p = czero();
+#pragma unroll
+  for (int j = 0; j < L; ++j)
+    if (j < Lk) {
+      p = cfma(cf.r2, p, d[j]);
+      d[j] = p;
+    }
+  double2 tot;
+  const double2 vin = warp_affine_scan<false>(p, cf.r2L, &tot);
+  double2 rp = cf.r2;  // r2^{j+1}
+#pragma unroll
+  for (int j = 0; j < L; ++j)
+    if (j < Lk) {
+      d[j] = cfma(rp, vin, d[j]);
+      rp = cmul(rp, cf.r2);
+    }
+  // backward: x_i = s x_{i+1} - tau w_i (x_N = 0), and the response q to w_i = r2^{i+1} (same recurrence)
+  const double2 mtau = cneg(cf.tau);
+  const double2 B = cmul(mtau, cpow_small(cf.r2, i0 + 1));  // -tau r2^{i0+1}
+  double2 rq[L];  // -tau r2^{i+1} for the lane's rows
+  rq[0] = B;
+#pragma unroll
+  for (int j = 1; j < L; ++j) rq[j] = cmul(rq[j - 1], cf.r2);
+  p = czero();
+  double2 pq = czero();
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j)
+    if (j < Lk) {
+      p = cfma(cf.s, p, cmul(mtau, d[j]));
+      d[j] = p;
+      pq = cfma(cf.s, pq, rq[j]);
+      rq[j] = pq;
+    }
+  const double2 xin = warp_affine_scan<true>(p, cf.sL, &tot);
+  const double2 qin = warp_affine_scan<true>(pq, cf.sL, &tot);
+  double2 sp = make_double2(1.0, 0.0);  // s^{Lk - j}, built from the top row down
+#pragma unroll
+  for (int j = L - 1; j >= 0; --j)
+    if (j < Lk) {
+      sp = cmul(sp, cf.s);
+      d[j] = cfma(sp, xin, d[j]);
+      rq[j] = cfma(sp, qin, rq[j]);
+    }
+  // x_0 = x^(d)_0 / (1 - c q_0);  x_i += (c x_0) q_i
+  const double2 cx0 = cmul(cf.c, cmul(shfl2(d[0], 0), cf.g));
+#pragma unroll
+  for (int j = 0; j < L; ++j) d[j] = cscale(cfma(cx0, rq[j], d[j]), scale);
+#pragma unroll
+  for (int j = 0; j < L; ++j)
+    if (j < Lk) col[j] = d[j];
+  __syncthreads();
+#pragma unroll 4
+  for (int i = threadIdx.x; i < N * kYC; i += 32 * kYC) {
+    const int r = i / kYC, c = i % kYC;
+    if (c0 + c < N) __stcs(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
+  }
+}
+
+template <int M>
+cudaError_t dst_dtri_n(double2* Sh, int nfreq, int f0g, const pd_dtri_coef* coef, const double2* tw, int chunk,
+                       cudaStream_t st, int* launches) {
+  using T = SlabCfg<M>;
+  constexpr int N = M / 2 - 1, N1 = N + 1;
+  const int smr = smem_bytes<M>(), smd = kYC * (N1 + 33) * (int)sizeof(double2);
+  static int attr = -1;  // device on which the attributes were set
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (attr != dev_) {
+    cudaError_t e = cudaFuncSetAttribute(dst_rows_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dst_rows_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smr);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dtri_kernel<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smd);
+    if (e != cudaSuccess) return e;
+    attr = dev_;
+  }
+  int nl = 0;
+  for (int s0 = 0; s0 < nfreq; s0 += chunk) {
+    const int ns = nfreq - s0 < chunk ? nfreq - s0 : chunk;
+    double2* base = Sh + (long long)s0 * N * N;
+    const long long nrows = (long long)ns * N;
+    const unsigned row_ctas = (unsigned)((nrows + T::C - 1) / T::C);
+    dst_rows_kernel<M, false><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+    dtri_kernel<N1><<<dim3((N + kYC - 1) / kYC, ns), 32 * kYC, smd, st>>>(Sh, s0, f0g + s0, coef, 1.0 / M);
+    dst_rows_kernel<M, true><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+    nl += 3;
+  }
+  if (launches) *launches = nl;
+  return cudaGetLastError();
+}
+
 template <int N>
 cudaError_t filter_n(double2* slab, const double2* tab, const double2* tw, cudaStream_t st) {
   using T = SlabCfg<N>;
@@ -634,6 +765,20 @@ cudaError_t pd_launch_slab2d_dst(double2* Sh, int n, int nfreq, const double2* l
     case 127: return dst_n<256>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
     case 255: return dst_n<512>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
     case 511: return dst_n<1024>(Sh, nfreq, lam1, lam2, mu, tw, chunk, st, launches);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int pd_slab2d_dtri_supported(int n) { return n == 31 || n == 63 || n == 127 || n == 255 || n == 511; }
+
+cudaError_t pd_launch_slab2d_dtri(double2* Sh, int n, int nfreq, int f0_glob, const pd_dtri_coef* coef,
+                                  const double2* tw, int chunk, cudaStream_t st, int* launches) {
+  switch (n) {
+    case 31: return dst_dtri_n<64>(Sh, nfreq, f0_glob, coef, tw, chunk, st, launches);
+    case 63: return dst_dtri_n<128>(Sh, nfreq, f0_glob, coef, tw, chunk, st, launches);
+    case 127: return dst_dtri_n<256>(Sh, nfreq, f0_glob, coef, tw, chunk, st, launches);
+    case 255: return dst_dtri_n<512>(Sh, nfreq, f0_glob, coef, tw, chunk, st, launches);
+    case 511: return dst_dtri_n<1024>(Sh, nfreq, f0_glob, coef, tw, chunk, st, launches);
     default: return cudaErrorInvalidValue;
   }
 }

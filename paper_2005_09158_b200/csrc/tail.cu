@@ -9,6 +9,11 @@
 //            ow_n hc_n = m_n gamma_{Nt-1}^{-1} / Nt exp(2 pi i n (Nt-1) / Nt) (hc_n = gamma_0 = 1; m_n = half-spectrum
 //            multiplicity).  Computed once per context (F N^2 complex divisions, fixed order).
 //   r2c / take_real: real head <-> complex slab for the 2D filter (slab2d.cu pd_launch_slab2d_filter).
+//   2D Dirichlet (leapfrog, H = 2): K = -nu Lap_h is diagonal in the tensor DST-I basis (Y = S X S, S_jk =
+//            sin(pi jk/(N+1)), S^-1 = 2/(N+1) S), so tail_a = S^-1 [ sum_t tau_at . (S g_t S) ] S^-1 with the REAL
+//              tau_at(kx, ky) = Re sum_{n < F} ow_n[a] hc_n[t] / (lambda_1n + lambda_2n (mu_kx + mu_ky))
+//            (the tail map takes Re of the half-spectrum sum and S g S is real).  The DSTs are dense N x N products
+//            (N <= 511: 2 N^3 FMAs per transform, microseconds), tiled in shared memory.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -106,6 +111,94 @@ unsigned grid_for(long long n, int threads) {
 }
 
 }  // namespace
+
+namespace {
+
+__global__ void tau_dir_kernel(double* __restrict__ tau, int N, int F, int H, const double2* __restrict__ lam1,
+                               const double2* __restrict__ lam2, const double2* __restrict__ w,
+                               const double* __restrict__ mu) {
+  const long long NN = (long long)N * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NN; i += (long long)gridDim.x * blockDim.x) {
+    const int kx = (int)(i % N), ky = (int)(i / N);
+    const double m = mu[kx + 1] + mu[ky + 1];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int n = 0; n < F; ++n) {
+      const double2 den = cfma(lam2[n], make_double2(m, 0.0), lam1[n]);
+      const double2 inv = crcp(den);
+      for (int at = 0; at < H * H; ++at) {
+        const double2 wv = w[(long long)at * F + n];
+        acc[at] += wv.x * inv.x - wv.y * inv.y;  // Re(w / den)
+      }
+    }
+    for (int at = 0; at < H * H; ++at) tau[(long long)at * NN + i] = acc[at];
+  }
+}
+
+// out^T = in . S  (in, out: N x N row-major; S symmetric), 32 x 32 output tiles, 32 x 8 threads (4 outputs each)
+__global__ void dst_mm_t_kernel(const double* __restrict__ in, const double* __restrict__ S, double* __restrict__ out,
+                                int N) {
+  __shared__ double a[32][33], b[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = 0; k0 < N; k0 += 32) {
+    for (int q = 0; q < 4; ++q) {
+      const int r = ty + 8 * q;
+      a[r][tx] = (r0 + r < N && k0 + tx < N) ? in[(long long)(r0 + r) * N + k0 + tx] : 0.0;
+      b[r][tx] = (k0 + r < N && c0 + tx < N) ? S[(long long)(k0 + r) * N + c0 + tx] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k)
+      for (int q = 0; q < 4; ++q) acc[q] = fma(a[ty + 8 * q][k], b[k][tx], acc[q]);
+    __syncthreads();
+  }
+  // out[c][r] = (in S)[r][c]: stage through smem for coalesced stores
+  for (int q = 0; q < 4; ++q) a[ty + 8 * q][tx] = acc[q];
+  __syncthreads();
+  for (int q = 0; q < 4; ++q) {
+    const int c = ty + 8 * q;
+    if (c0 + c < N && r0 + tx < N) out[(long long)(c0 + c) * N + r0 + tx] = a[tx][c];
+  }
+}
+
+// out_a = scale * sum_t tau_at . G_t  (a < H)
+__global__ void tau_combine_kernel(const double* __restrict__ tau, const double* __restrict__ G, double* __restrict__ out,
+                                   long long NN, int H, double scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NN; i += (long long)gridDim.x * blockDim.x)
+    for (int a = 0; a < H; ++a) {
+      double v = 0.0;
+      for (int t = 0; t < H; ++t) v = fma(tau[(long long)(a * H + t) * NN + i], G[(long long)t * NN + i], v);
+      out[(long long)a * NN + i] = scale * v;
+    }
+}
+
+}  // namespace
+
+cudaError_t pd_launch_tau_dir(double* tau, int n, int nfreq, int H, const double2* lam1, const double2* lam2,
+                              const double2* w, const double* mu, cudaStream_t st) {
+  tau_dir_kernel<<<grid_for((long long)n * n, 128), 128, 0, st>>>(tau, n, nfreq, H, lam1, lam2, w, mu);
+  return cudaGetLastError();
+}
+
+// 2D DST-I of H real N x N blocks, both directions (Y = S X S): two transposing products per block via tmp
+cudaError_t pd_launch_dst2d_dense(const double* in, double* out, double* tmp, const double* S, int N, int H,
+                                  cudaStream_t st) {
+  const dim3 grid((N + 31) / 32, (N + 31) / 32), block(32, 8);
+  const long long NN = (long long)N * N;
+  for (int t = 0; t < H; ++t) {
+    dst_mm_t_kernel<<<grid, block, 0, st>>>(in + t * NN, S, tmp, N);
+    dst_mm_t_kernel<<<grid, block, 0, st>>>(tmp, S, out + t * NN, N);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t pd_launch_tau_combine(const double* tau, const double* G, double* out, int N, int H, double scale,
+                                  cudaStream_t st) {
+  const long long NN = (long long)N * N;
+  tau_combine_kernel<<<grid_for(NN, 256), 256, 0, st>>>(tau, G, out, NN, H, scale);
+  return cudaGetLastError();
+}
 
 cudaError_t pd_launch_head_G(const pd_stencil& p, const pd_tail_g& gc, const double* tail, double* head, long long S,
                              cudaStream_t st) {

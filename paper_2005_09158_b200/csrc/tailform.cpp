@@ -68,7 +68,6 @@ namespace {
 pd_status tail_setup(pd_ctx* c) {
   auto& T = c->tail;
   if (T.ready) return PD_OK;
-  if (c->g.op == PD_WAVE2D_DIRICHLET) return fail(c, PD_EINVAL, "tail form: not built for the 2D Dirichlet operator");
   if (c->use_gtsv)
     return fail(c, PD_EINVAL, "tail form: the 1D tail map needs the recurrence Step (b) (context uses pivoted elimination)");
   const int H = c->scheme == PD_LEAPFROG ? 2 : 1;
@@ -114,6 +113,32 @@ pd_status tail_setup(pd_ctx* c) {
     PD_LAUNCH(c, pd_launch_tau2d(T.tau, N, F, c->lam1, c->lam2, wd, c->sx, c->sn, c->slab, c->st));
     PD_CUDA(c, cudaStreamSynchronize(c->st));
     cudaFree(wd);
+  } else if (c->g.op == PD_WAVE2D_DIRICHLET) {
+    // tensor DST-I basis: real transfer tables tau[a][t][ky][kx] (tail.cu tau_dir), the N x N sine table
+    const int N = c->g.nx;
+    const long long NN = (long long)N * N;
+    std::vector<double2> wat((size_t)H * H * F);
+    for (int a = 0; a < H; ++a)
+      for (int t = 0; t < H; ++t)
+        for (int n = 0; n < F; ++n) {
+          const cld v = cld(ow[(size_t)n * H + a].x, ow[(size_t)n * H + a].y) * cld(hc[(size_t)n * H + t].x,
+                                                                                  hc[(size_t)n * H + t].y);
+          wat[((size_t)a * H + t) * F + n] = make_double2((double)v.real(), (double)v.imag());
+        }
+    double2* wd = nullptr;
+    PD_CUDA(c, dalloc_c(&wd, wat.size()));
+    PD_CUDA(c, cudaMemcpy(wd, wat.data(), wat.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    PD_CUDA(c, dalloc_d(&T.taud, (size_t)H * H * NN));
+    PD_LAUNCH(c, pd_launch_tau_dir(T.taud, N, F, H, c->lam1, c->lam2, wd, c->mu, c->st));
+    PD_CUDA(c, cudaStreamSynchronize(c->st));
+    cudaFree(wd);
+    std::vector<double> sn((size_t)NN);
+    for (int j = 0; j < N; ++j)
+      for (int k = 0; k < N; ++k)
+        sn[(size_t)j * N + k] = (double)sinl(pi * (long double)((j + 1) * (long long)(k + 1) % (2 * (N + 1))) / (N + 1));
+    PD_CUDA(c, dalloc_d(&T.dsin, (size_t)NN));
+    PD_CUDA(c, cudaMemcpy(T.dsin, sn.data(), sn.size() * sizeof(double), cudaMemcpyHostToDevice));
+    PD_CUDA(c, dalloc_d(&T.dwork, (size_t)(2 * H + 1) * NN));
   } else {
     PD_CUDA(c, dalloc_c(&T.ow, (size_t)F * H));
     PD_CUDA(c, cudaMemcpy(T.ow, ow.data(), ow.size() * sizeof(double2), cudaMemcpyHostToDevice));
@@ -170,6 +195,17 @@ pd_status comb(pd_ctx* c, std::vector<const double*> X, std::vector<double> coef
 pd_status tail_map(pd_ctx* c, const double* g, double* out) {
   auto& T = c->tail;
   const long long Sg = c->Sg, Hn = (long long)T.H * Sg;
+  if (c->g.op == PD_WAVE2D_DIRICHLET) {  // every rank: S^-1 [sum_t tau_at . (S g_t S)] S^-1 on the whole head
+    const int N = c->g.nx;
+    const long long NN = (long long)N * N;
+    double *G = T.dwork, *Ta = T.dwork + T.H * NN, *tmp = T.dwork + 2 * T.H * NN;
+    PD_CUDA(c, pd_launch_dst2d_dense(g, G, tmp, T.dsin, N, T.H, c->st));
+    const double sc = 2.0 / (N + 1);
+    PD_CUDA(c, pd_launch_tau_combine(T.taud, G, Ta, N, T.H, sc * sc, c->st));
+    PD_CUDA(c, pd_launch_dst2d_dense(Ta, out, tmp, T.dsin, N, T.H, c->st));
+    c->launches += 4 * T.H + 1;
+    return PD_OK;
+  }
   if (c->g.op == PD_ADE2D_PERIODIC) {  // every rank: one slab FFT filter of the whole head
     PD_LAUNCH(c, pd_launch_r2c(g, T.work, Sg, c->st));
     PD_CUDA(c, pd_launch_slab2d_filter(T.work, c->g.nx, T.tau, c->tw_s, c->st));
@@ -270,7 +306,7 @@ pd_status zero_report(pd_ctx* c, double* u, pd_report* rep) {
 void pd_tail_free(pd_ctx* c) {
   auto& T = c->tail;
   for (void* p : {(void*)T.hc, (void*)T.ow, (void*)T.part, (void*)T.tau, (void*)T.work, (void*)T.flag, (void*)T.acc,
-                  (void*)T.gx})
+                  (void*)T.gx, (void*)T.taud, (void*)T.dsin, (void*)T.dwork})
     if (p) cudaFree(p);
   for (double* p : T.scr) cudaFree(p);
   for (double* p : T.Vh) cudaFree(p);

@@ -38,9 +38,10 @@ SMALL = [
     (W.ADE2D, W.BE, 32, 1024), (W.ADE2D, W.CN, 64, 1024), (W.ADE2D, W.CN, 32, 4096),
     # every x-FFT pass plan of the x-first kernels: NP = 64 (16, 4), 128 (16, 8); NX = 1024 via the slab route
     (W.ADE2D, W.CN, 128, 1024), (W.ADE2D, W.BE, 256, 1024), (W.ADE2D, W.BE, 1024, 2),
-    # 2D homogeneous Dirichlet (Table T4A operator): tensor DST-I via odd-extension FFTs, ragged column tiles
+    # 2D homogeneous Dirichlet (Table T4A operator): x-DST-I via odd-extension FFTs, y by Dirichlet Toeplitz
+    # recurrences (N + 1 >= 32; N = 15 keeps the DST column pass), ragged column tiles (N = 2^k - 1 columns)
     (W.WAVE2D, W.LF, 15, 16), (W.WAVE2D, W.LF, 31, 64), (W.WAVE2D, W.LF, 63, 1024), (W.WAVE2D, W.BE, 31, 8),
-    (W.WAVE2D, W.LF, 255, 4),
+    (W.WAVE2D, W.LF, 255, 4), (W.WAVE2D, W.LF, 127, 128), (W.WAVE2D, W.CN, 511, 4), (W.WAVE2D, W.LF, 255, 256),
     # Nt = 1 (S:l.89, reading t2): one plain solve (c1 I + c2 K) z = r, no wrap entry
     (W.ADE1D, W.BE, 63, 1), (W.ADE1D, W.CN, 4095, 1), (W.ADE2D, W.CN, 32, 1), (W.WAVE2D, W.BE, 31, 1),
 ]
@@ -70,6 +71,18 @@ def test_apply_matches_oracle_small(op, scheme, nx, nt):
     r = W.random_vector(cfg, seed=nx * 7 + nt)
     ctx = make_ctx(cfg)
     z = to_host(ctx.apply_precond(to_dev(r)))
+    check_apply(cfg, r, z)
+
+
+@pytest.mark.parametrize("op,scheme,nx,nt", [(W.WAVE2D, W.LF, 31, 64), (W.WAVE2D, W.LF, 255, 16),
+                                             (W.WAVE2D, W.BE, 63, 8)])
+def test_apply_2d_dirichlet_dst_column_pass_matches_oracle(monkeypatch, op, scheme, nx, nt):
+    """PD_NO_DTRI=1: the y-direction by the DST column pass (FFT of the odd extension -> divide -> IFFT) instead of
+    the Dirichlet Toeplitz recurrences (env read at context setup)."""
+    monkeypatch.setenv("PD_NO_DTRI", "1")
+    cfg = _cfg(op, scheme, nx, nt, alpha=0.02)
+    r = W.random_vector(cfg, seed=nx + nt)
+    z = to_host(make_ctx(cfg).apply_precond(to_dev(r)))
     check_apply(cfg, r, z)
 
 

@@ -19,6 +19,9 @@ MAP_CASES = [
     W.CONFIGS[1].scaled(nx=17, nt=8),                    # tiny, one warp, F < grid
     W.CONFIGS[3].scaled(nx=32, ny=32, nt=64),            # 2D periodic, transfer function
     W.CONFIGS[4].scaled(nx=32, ny=32, nt=1024),          # 2D, tfx context (x-FFT folded into the time FFT)
+    W.t4a_config(32),                                    # 2D Dirichlet leapfrog (H = 2): DST-I transfer tables
+    W.t4a_config(64, 1.0),                               # 2D Dirichlet, alpha = 1 (resonant), 63 x 63 (ragged tiles)
+    W.t4a_config(32).scaled(scheme=W.CN),                # 2D Dirichlet theta-method (H = 1)
 ]
 
 
@@ -158,10 +161,24 @@ def test_tail_sharded_virtual_ranks(name, P):
     assert rel(to_host(u), u_ref) < SOLVE_TOL
 
 
-def test_tail_rejects_2d_dirichlet():
-    cfg = W.t4a_config(32)
+@pytest.mark.parametrize("label,alpha", [(32, 0.1), (64, 0.1), (128, 0.1), (32, 1.0)])
+def test_tail_gmres_2d_dirichlet_matches_oracle(label, alpha):
+    """Table T4A in tail form (NEXT-3 with NEXT-1): GMRES on the head/tail reduced problem takes the residual-form
+    oracle's iteration count and solution (alpha = 1: the count pinned per mesh as in test_t4a, reading x4)."""
+    cfg = W.t4a_config(label, alpha)
     ctx = make_ctx(cfg)
-    from paper_2005_09158_b200 import ParaDiagError
-    with pytest.raises(ParaDiagError):
-        ctx.tail_map(to_dev(np.zeros((2, cfg.S))))
-    # (Nt >= 2H is already required by pd_setup: Nt >= 2 for the theta-method, >= 4 for leapfrog)
+    b_dev, b = _rhs(ctx, cfg)
+    u, rep = ctx.solve_gmres_tail(b_dev, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit)
+    u_ref, rep_ref = solvers.solve_gmres(cfg, b)
+    assert rep.converged
+    if alpha < 1.0:
+        assert rep.iterations == rep_ref.iterations
+        assert rel(to_host(u), u_ref) < SOLVE_TOL
+    else:  # reading x4: within the range of the three references of tests/golden/t4a_alpha1_counts.json
+        import json
+        import os
+        with open(os.path.join(os.path.dirname(__file__), "golden", "t4a_alpha1_counts.json")) as fh:
+            runs = json.load(fh)["runs"]
+        refs = [runs[f"{label}_{n}"]["iterations"] for n in ("O1_fp64", "O2_fp64", "O2_longdouble")]
+        assert min(refs) <= rep.iterations <= max(refs), (rep.iterations, refs)
+        assert np.linalg.norm(problems.matvec_A(cfg, to_host(u)) - b) <= 1.01 * cfg.tol * np.linalg.norm(b)
