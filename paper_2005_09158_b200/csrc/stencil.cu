@@ -5,6 +5,8 @@
 // previous rows in registers; per-block partial sums of r^2 feed a deterministic fixed-order reduction.
 // Also the right-hand side b of A u = b from (U_0, V_0, f) (readings c4, c5).
 #include "common.cuh"
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace {
@@ -247,6 +249,129 @@ __global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_kernel(
   }
 }
 
+// Two x-points per lane (16-byte loads and stores, 64 x-points per warp tile): the same walk as stencil2d_kernel with
+// twice the bytes in flight per lane and half the instructions per point (needs nx % 64 == 0 and 16-byte aligned
+// vectors).  Component 0 (x) takes its left neighbour from lane - 1's component 1 and its right one from its own
+// component 1; component 1 (x + 1) the mirror image.
+template <int NT>
+__global__ void __launch_bounds__(32 * kW2, PD_STENCIL2D_MINB) stencil2d_v2_kernel(pd_stencil p, const double* __restrict__ b,
+                                                                const double* __restrict__ u, double* __restrict__ out,
+                                                                double* __restrict__ partial) {
+  __shared__ double2 ysh[2][kW2][32];
+  __shared__ double red[kW2];
+  const int nx = p.nx, ny = p.ny;
+  const long long S = (long long)nx * ny;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * 64, y0 = blockIdx.y * kTY;
+  const int ylast = min(y0 + kTY, ny) - 1;
+  const int x = x0 + 2 * lane;
+  int srow = 0, y = 0;
+  const double* hsrc = nullptr;
+  if (warp < kTY) {
+    y = y0 + warp;
+    srow = warp + 1;
+  }
+  const bool per = p.op == 2;
+  bool zrow = false;
+  if (warp == kTY) {
+    y = y0 - 1;
+    srow = 0;
+    if (y < 0) {
+      y = ny - 1;
+      hsrc = p.hlo;
+      zrow = !per && !hsrc;
+    }
+  } else if (warp > kTY) {
+    y = ylast + 1;
+    srow = ylast - y0 + 2;
+    if (y >= ny) {
+      y = 0;
+      hsrc = p.hhi;
+      zrow = !per && !hsrc;
+    }
+  }
+  const bool act = warp < kTY && y <= ylast;
+  const bool live = (warp >= kTY && !zrow) || (warp < kTY && y <= ylast);
+  const bool needL = act && lane == 0, needR = act && lane == 31;
+  const int xl = x == 0 ? nx - 1 : x - 1, xr = x + 2 == nx ? 0 : x + 2;
+  const double* rowp = hsrc ? hsrc : u + (long long)y * nx;
+  const long long rstride = hsrc ? nx : S;
+  const int n0 = blockIdx.z * kTC;
+  const int n1 = min(n0 + kTC, p.nt);
+  const double* pc = rowp + (long long)n0 * rstride + x;
+  const int dl = xl - x, dr = xr - x;
+  auto ld2 = [&](const double* q, int n) -> double2 {
+    return (n >= 0 && live) ? *reinterpret_cast<const double2*>(q) : make_double2(0.0, 0.0);
+  };
+  auto ld1 = [&](const double* q, int n, int d) -> double { return (n >= 0 && live) ? q[d] : 0.0; };
+  double2 c0 = make_double2(0.0, 0.0), c1 = ld2(pc - rstride, n0 - 1),
+          c2 = NT == 3 ? ld2(pc - 2 * rstride, n0 - 2) : make_double2(0.0, 0.0);
+  Hist L = {0.0, 0.0, 0.0}, R = {0.0, 0.0, 0.0};
+  const bool ldL = needL && (per || x != 0), ldR = needR && (per || x + 1 != nx - 1);  // Dirichlet: 0 outside
+  if (ldL) { L.h1 = ld1(pc - rstride, n0 - 1, dl); if (NT == 3) L.h2 = ld1(pc - 2 * rstride, n0 - 2, dl); }
+  if (ldR) { R.h1 = ld1(pc - rstride, n0 - 1, dr); if (NT == 3) R.h2 = ld1(pc - 2 * rstride, n0 - 2, dr); }
+  const long long off = (long long)n0 * S + (long long)y * nx + x;
+  const double* pb = b ? b + off : nullptr;
+  const bool wr = out != nullptr;
+  double* po = wr ? out + off : nullptr;
+  double2 nc = live ? *reinterpret_cast<const double2*>(pc) : make_double2(0.0, 0.0);
+  double nl = ldL ? pc[dl] : 0.0, nr = ldR ? pc[dr] : 0.0;
+  double2 nb = (act && pb) ? *reinterpret_cast<const double2*>(pb) : make_double2(0.0, 0.0);
+  double acc = 0.0;
+  int buf = 0;
+  auto cmb = [&](double h0, double h1, double h2) {
+    return NT == 3 ? p.c2[0] * h0 + p.c2[1] * h1 + p.c2[2] * h2 : p.c2[0] * h0 + p.c2[1] * h1;
+  };
+  auto cmb1 = [&](double h0, double h1, double h2) {
+    return NT == 3 ? p.c1[0] * h0 + p.c1[1] * h1 + p.c1[2] * h2 : p.c1[0] * h0 + p.c1[1] * h1;
+  };
+  for (int n = n0; n < n1; ++n) {
+    c0 = nc;
+    L.h0 = nl;
+    R.h0 = nr;
+    const double2 bv = nb;
+    if (n + 1 < n1) {
+      pc += rstride;
+      if (live) nc = *reinterpret_cast<const double2*>(pc);
+      if (ldL) nl = pc[dl];
+      if (ldR) nr = pc[dr];
+      if (act && pb) nb = *reinterpret_cast<const double2*>(pb + S);
+    }
+    const double2 yc = make_double2(cmb(c0.x, c1.x, c2.x), cmb(c0.y, c1.y, c2.y));
+    if (live || warp >= kTY) ysh[buf][srow][lane] = yc;
+    const double up = __shfl_up_sync(0xffffffffu, yc.y, 1);
+    const double dn = __shfl_down_sync(0xffffffffu, yc.x, 1);
+    const double yxm0 = needL ? cmb(L.h0, L.h1, L.h2) : up;
+    const double yxp1 = needR ? cmb(R.h0, R.h1, R.h2) : dn;
+    __syncthreads();
+    if (act) {
+      const double2 yym = ysh[buf][srow - 1][lane], yyp = ysh[buf][srow + 1][lane];
+      double a0 = cmb1(c0.x, c1.x, c2.x), a1 = cmb1(c0.y, c1.y, c2.y);
+      a0 += p.k2c * yc.x + p.k2x_m * yxm0 + p.k2x_p * yc.y + p.k2y_m * yym.x + p.k2y_p * yyp.x;
+      a1 += p.k2c * yc.y + p.k2x_m * yc.x + p.k2x_p * yxp1 + p.k2y_m * yym.y + p.k2y_p * yyp.y;
+      const double v0 = pb ? bv.x - a0 : a0, v1 = pb ? bv.y - a1 : a1;
+      if (wr) *reinterpret_cast<double2*>(po) = make_double2(v0, v1);
+      acc = fma(v0, v0, acc);
+      acc = fma(v1, v1, acc);
+    }
+    if (wr) po += S;
+    if (pb) pb += S;
+    c2 = c1;
+    c1 = c0;
+    L.h2 = L.h1; L.h1 = L.h0;
+    R.h2 = R.h1; R.h1 = R.h0;
+    buf ^= 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kTY; ++w) t += red[w];
+    partial[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 // ---------------- right-hand side ----------------
 // K v at spatial point s of a single time level (zero Dirichlet / periodic wrap)
 // 2D homogeneous Dirichlet neighbourhood (zero outside; halo rows of neighbour ranks in y)
@@ -317,11 +442,20 @@ cudaError_t pd_launch_stencil(const pd_stencil& p, const double* b, const double
                               int* nblocks_out, cudaStream_t st) {
   if (nblocks_out) *nblocks_out = pd_stencil_num_blocks(p);
   if (p.op >= 2) {
-    dim3 grid((unsigned)((p.nx + 31) / 32), (unsigned)((p.ny + kTY - 1) / kTY), (unsigned)((p.nt + kTC - 1) / kTC));
     pd_stencil q = p;
     const Taps t = taps_host(p);
     for (int k = 0; k < 3; ++k) { q.c1[k] = t.c1[k]; q.c2[k] = t.c2[k]; }
-    if (t.ntaps == 3)
+    auto al = [](const void* v) { return (reinterpret_cast<uintptr_t>(v) & 15) == 0; };
+    static const bool v1_only = getenv("PD_STENCIL_V1") != nullptr;
+    const bool v2 = !v1_only && p.nx % 64 == 0 && al(u) && al(b) && al(out) && al(p.hlo) && al(p.hhi);
+    const int tw = v2 ? 64 : 32;
+    dim3 grid((unsigned)((p.nx + tw - 1) / tw), (unsigned)((p.ny + kTY - 1) / kTY), (unsigned)((p.nt + kTC - 1) / kTC));
+    if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y * grid.z);
+    if (v2 && t.ntaps == 3)
+      stencil2d_v2_kernel<3><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
+    else if (v2)
+      stencil2d_v2_kernel<2><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
+    else if (t.ntaps == 3)
       stencil2d_kernel<3><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
     else
       stencil2d_kernel<2><<<grid, 32 * kW2, 0, st>>>(q, b, u, out, partial);
