@@ -108,6 +108,7 @@ struct pd_ctx {
   int gm_m = 0;
   std::vector<double*> V;
   double* zvec = nullptr;
+  std::vector<double*> Zs;       // GMRES: Z_j = P^{-1} X_j of the current cycle (final assembly by one sweep)
   double* gm_head = nullptr;     // head-sized work vector of the corner-identity GMRES path
   double* gm_full = nullptr;     // NCCL ranks: replicated [H][S_glob] tail and head of the corner identity
   int* gm_flag = nullptr;        // zero-initial-guess check

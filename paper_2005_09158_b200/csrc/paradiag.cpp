@@ -220,6 +220,7 @@ static void free_ctx(pd_ctx* c) {
   if (c->nl_dbar) cudaFree(c->nl_dbar);
   if (c->gm_head) cudaFree(c->gm_head);
   if (c->gm_full) cudaFree(c->gm_full);
+  for (double* p : c->Zs) cudaFree(p);
   if (c->gm_flag) cudaFree(c->gm_flag);
   if (c->ivp_init) cudaFree(c->ivp_init);
   if (c->ivp_f) cudaFree(c->ivp_f);
@@ -1040,6 +1041,28 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     }
     c->gm_m = m;
   }
+  // Z_j = P^{-1} X_j kept for the final assembly u = x0 + sum_j y_j sc_j Z_j (the applies write them anyway), which
+  // replaces the final apply P^{-1}(V y) by one combination sweep; only if the m extra vectors fit with 2 GB to spare
+  // (PD_GMRES_NO_Z=1: the final apply)
+  bool useZ = getenv("PD_GMRES_NO_Z") == nullptr && (reinterpret_cast<uintptr_t>(u) & 15) == 0;
+  if (useZ && (int)c->Zs.size() < m) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = (size_t)(m - (int)c->Zs.size()) * (size_t)n * sizeof(double) + (2ull << 30);
+    if (fr < need) {
+      useZ = false;
+    } else {
+      while ((int)c->Zs.size() < m) {
+        double* p = nullptr;
+        if (dalloc(&p, (size_t)n) != cudaSuccess) {
+          cudaGetLastError();
+          useZ = false;
+          break;
+        }
+        c->Zs.push_back(p);
+      }
+    }
+  }
   const double* Xb[1] = {b};
   double bb = 0;
   pd_status s = dots_impl(c, Xb, 1, b, &bb);
@@ -1108,7 +1131,8 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     int kk = 0;
     for (int j = 0; j < m; ++j) {
       // w_raw = A P^{-1} X_j;  true w = sc[j] * w_raw
-      s = pd_apply_impl(c, Xv[j], c->zvec, 0);
+      double* zj = useZ ? c->Zs[j] : c->zvec;
+      s = pd_apply_impl(c, Xv[j], zj, 0);
       if (s != PD_OK) return s;
       ++its;
       double* w = c->V[j + 1];
@@ -1117,7 +1141,7 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
         // behind the tail form): the matvec sweep disappears and, the basis being orthonormal, the first CGS pass is
         // h_i = delta_ij - sc_i sc_j <X_i[head], G tail>: head-only dots.  The second pass measures the true
         // projections of the assembled w as before, so orthogonality is enforced to working precision.
-        s = pd_corner_head(c, gcorner, c->zvec + (long long)(c->nt - gcorner.H) * c->S, dhead);
+        s = pd_corner_head(c, gcorner, zj + (long long)(c->nt - gcorner.H) * c->S, dhead);
         if (s != PD_OK) return s;
         s = pd_krylov_n(c, 0, Xp, nullptr, j + 1, 0.0, dhead, hn_len, eh.data());  // <X_i[head], G tail>
         if (s != PD_OK) return s;
@@ -1155,7 +1179,7 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
           }
         }
       } else {
-        s = pd_stencil_impl(c, nullptr, c->zvec, w, nullptr);
+        s = pd_stencil_impl(c, nullptr, zj, w, nullptr);
         if (s != PD_OK) return s;
         // CGS2: h_i = <V_i, w> = sc_i sc_j <X_i, w_raw>;  w_raw -= sum (h_i sc_i / sc_j) X_i  (fused with 2nd dots)
         s = krylov_impl(c, 0, Xp, nullptr, j + 1, 0.0, w, h.data());
@@ -1211,8 +1235,20 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
       y[i] = t / Hs(i, i);
     }
     for (int i = 0; i < kk; ++i) coef[i] = y[i] * sc[i];
+    const int acc0 = u_is_zero ? 0 : 1;
+    if (useZ) {  // u (+)= sum_i coef_i Z_i: one sweep over kk + 1 vectors instead of an apply
+      u_is_zero = false;
+      std::vector<const double*> Zp(c->Zs.begin(), c->Zs.begin() + kk);
+      if (acc0 == 0) {
+        s = krylov_impl(c, 3, Zp.data(), coef.data(), kk, 0.0, u, nullptr);
+      } else {
+        double unused = 0;
+        s = krylov_impl(c, 2, Zp.data(), coef.data(), kk, 1.0, u, &unused);
+      }
+      if (s != PD_OK) return s;
+    }
     // fused: the forward time FFT reads the basis combination itself (tfx path, single GPU, no graphs)
-    bool fused = c->use_tfx && c->dist_mode == 0 && !c->use_graphs && kk <= kPdCombMax && c->S % 2 == 0 &&
+    bool fused = !useZ && c->use_tfx && c->dist_mode == 0 && !c->use_graphs && kk <= kPdCombMax && c->S % 2 == 0 &&
                  getenv("PD_GMRES_NO_FUSED_UPDATE") == nullptr;
     pd_comb_args cb{};
     for (int i = 0; fused && i < kk; ++i) {
@@ -1223,7 +1259,9 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     cb.k = kk;
     const int acc = u_is_zero ? 0 : 1;  // u = 0: u + x == x exactly, so write x (no read of u)
     u_is_zero = false;
-    if (fused) {
+    if (useZ) {
+      // assembled above
+    } else if (fused) {
       s = apply_comb_accumulate(c, &cb, u, acc);
       if (s != PD_OK) return s;
     } else {
