@@ -101,6 +101,7 @@ struct pd_ctx {
   double2* Sh = nullptr;         // half spectrum [F][S] complex (frequency-sharded layout when size > 1)
   double* rvec = nullptr;        // residual / temp vector
   double* partial = nullptr;     // reduction partials
+  double* npart = nullptr;       // per-CTA partial sums of ||b||^2 fused into the first GMRES apply
   int npartial = 0;
   double* dred = nullptr;        // reduced scalars (device)
   double* hred = nullptr;        // pinned host scalars

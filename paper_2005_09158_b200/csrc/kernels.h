@@ -127,7 +127,9 @@ cudaError_t pd_launch_tf4_fwd_s1_tma(int nt, const double* r, long long S, long 
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, const pd_spec& sp, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr,
-                              const pd_comb_args* comb = nullptr);  // comb: r unused
+                              const pd_comb_args* comb = nullptr,  // comb: r unused
+                              double* npart = nullptr,            // non-NULL: per-CTA partial sums of r^2 too
+                              long long* nparts = nullptr);       // their count (the caller reduces in order)
 cudaError_t pd_launch_tfx_inv(int nt, int nx, const pd_spec& sp, double* z, long long S, const double* igam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
                               int accumulate, cudaStream_t st, int* nl, const pd_tfx_overlap* ov = nullptr);

@@ -220,6 +220,7 @@ static void free_ctx(pd_ctx* c) {
   if (c->nl_dbar) cudaFree(c->nl_dbar);
   if (c->gm_head) cudaFree(c->gm_head);
   if (c->gm_full) cudaFree(c->gm_full);
+  if (c->npart) cudaFree(c->npart);
   for (double* p : c->Zs) cudaFree(p);
   if (c->gm_flag) cudaFree(c->gm_flag);
   if (c->ivp_init) cudaFree(c->ivp_init);
@@ -828,6 +829,33 @@ static pd_status apply_comb_accumulate(pd_ctx* c, const pd_comb_args* cb, double
   return pd_time_fft_inv(c, pd_spec_local(c->Sh, c->S), u, c->S, accumulate);
 }
 
+// z = P^{-1} r with ||r||^2 taken by the forward time FFT's stage-1 loader (tfx path, single GPU): *rr on the host
+// (syncs).  PD_ECUDA-free fallback: returns PD_EINVAL when the fused form does not apply (caller uses dots + apply).
+static pd_status apply_with_norm(pd_ctx* c, const double* r, double* z, double* rr) {
+  const pd_tf4_tables tb{c->tw_n1, c->tw_n2, c->tw_t};
+  if (!c->npart) {  // one partial per stage-1 CTA: <= 8 (npairs / 8 + chunks) (tiles of >= 8 pairs, 8 t1 rows)
+    const long long npairs = c->S / 2, chunks = (npairs + c->tf4_chunk - 1) / c->tf4_chunk;
+    PD_CUDA(c, dalloc(&c->npart, (size_t)(8 * (npairs / 8 + chunks) + 64)));
+  }
+  phase_begin(c, 0);
+  int nl = 0;
+  long long np = 0;
+  PD_CUDA(c, pd_launch_tfx_fwd(c->nt, c->g.nx, r, pd_spec_local(c->Sh, c->S), c->S, c->gam, tb, c->tw_s,
+                               c->tf4_scratch, c->tf4_chunk, c->st, &nl, c->ov.k > 1 ? &c->ov : nullptr, nullptr,
+                               c->npart, &np));
+  c->launches += nl;
+  PD_LAUNCH(c, pd_launch_reduce_partials(c->npart, (int)np, 1, c->dred, c->st));
+  phase_end(c, 0);
+  pd_status s = pd_spatial_solve(c, c->Sh, c->F, 0);
+  if (s != PD_OK) return s;
+  s = pd_time_fft_inv(c, pd_spec_local(c->Sh, c->S), z, c->S, 0);
+  if (s != PD_OK) return s;
+  PD_CUDA(c, cudaMemcpyAsync(c->hred, c->dred, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  PD_CUDA(c, cudaStreamSynchronize(c->st));
+  *rr = c->hred[0];
+  return PD_OK;
+}
+
 // z = P^{-1} r, or u += P^{-1} r when accumulate.  With graphs enabled (single GPU, phase timing off) the
 // launch sequence of each (r, z, accumulate) triple is captured once and replayed as one CUDA graph.
 pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
@@ -1063,16 +1091,6 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
       }
     }
   }
-  const double* Xb[1] = {b};
-  double bb = 0;
-  pd_status s = dots_impl(c, Xb, 1, b, &bb);
-  if (s != PD_OK) return s;
-  const double bnorm = std::sqrt(bb);
-  if (bnorm == 0.0) {
-    PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * n, c->st));
-    if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
-    return PD_OK;
-  }
   // Basis kept scaled: V_i = sc[i] * X_i with X_i = c->V[i] in memory, so normalising costs no sweep.
   // Zero initial guess (checked on the device, single GPU): r0 = b exactly, so the first cycle reads X_0 = b in
   // place of a residual sweep; a restart writes the true residual into c->V[0].
@@ -1094,6 +1112,24 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     PD_CUDA(c, cudaStreamSynchronize(c->st));
     u_zero = *c->gm_hflag == 0;
   }
+  // ||b|| fused into the first apply's Step (a) read of b (zero initial guess, tfx path, single GPU): one sweep over
+  // b less per solve; the b = 0 / tol >= 1 exits are then taken after that apply
+  const bool fuse_bnorm = u_zero && maxit > 0 && c->dist_mode == 0 && c->use_tfx && !c->use_graphs && c->S % 2 == 0 &&
+                          (reinterpret_cast<uintptr_t>(b) & 15) == 0 && getenv("PD_GMRES_NO_FUSED_NORM") == nullptr;
+  const double* Xb[1] = {b};
+  double bb = 0;
+  pd_status s = PD_OK;
+  double bnorm = 1.0;  // set by the first apply when fuse_bnorm
+  if (!fuse_bnorm) {
+    s = dots_impl(c, Xb, 1, b, &bb);
+    if (s != PD_OK) return s;
+    bnorm = std::sqrt(bb);
+    if (bnorm == 0.0) {
+      PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * n, c->st));
+      if (rep) *rep = pd_report{0, 1, 0.0, 0.0, rep->history, rep->history_cap, 0};
+      return PD_OK;
+    }
+  }
   if (u_zero) {
     Xv[0] = b;
     rr = bb;
@@ -1103,7 +1139,8 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
   }
   double beta = std::sqrt(rr);
   int its = 0;
-  bool conv = beta <= tol * bnorm, breakdown = false;
+  bool conv = !fuse_bnorm && beta <= tol * bnorm, breakdown = false;
+  bool norm_pending = fuse_bnorm;  // u_zero holds (zero_guess with an aligned b): X_0 = b
   std::vector<double> H((m + 1) * m), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 2), y(m), coef(m + 1), sc(m + 1);
   auto Hs = [&](int i, int j) -> double& { return H[i * m + j]; };
   const double* const* Xp = Xv.data();
@@ -1132,8 +1169,24 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     for (int j = 0; j < m; ++j) {
       // w_raw = A P^{-1} X_j;  true w = sc[j] * w_raw
       double* zj = useZ ? c->Zs[j] : c->zvec;
-      s = pd_apply_impl(c, Xv[j], zj, 0);
-      if (s != PD_OK) return s;
+      if (norm_pending) {  // first apply of the solve: X_0 = b, ||b||^2 from its Step (a)
+        norm_pending = false;
+        s = apply_with_norm(c, Xv[0], zj, &bb);
+        if (s != PD_OK) return s;
+        bnorm = std::sqrt(bb);
+        rr = bb;
+        beta = bnorm;
+        if (bnorm == 0.0 || beta <= tol * bnorm) {  // b = 0, or tol >= 1: u = 0 solves it (no iteration counted)
+          PD_CUDA(c, cudaMemsetAsync(u, 0, sizeof(double) * n, c->st));
+          if (rep) *rep = pd_report{0, 1, bnorm == 0.0 ? 0.0 : 1.0, 0.0, rep->history, rep->history_cap, 0};
+          return PD_OK;
+        }
+        sc[0] = 1.0 / beta;
+        gv[0] = beta;
+      } else {
+        s = pd_apply_impl(c, Xv[j], zj, 0);
+        if (s != PD_OK) return s;
+      }
       ++its;
       double* w = c->V[j + 1];
       if (corner) {

@@ -10,12 +10,16 @@ using namespace pdfft;
 // forward stage 1 (N2 = stage length, KP pairs per tile): for fixed t1 (blockIdx.y): N2-point FFT over t2 of rows t1 + N1 t2 of P pairs,
 // times w_Nt^{t1 n2}; writes Y[t1][n2][pl] (scratch rows of Pc pairs).
 // ---------------------------------------------------------------------------------------------
-template <int NT, int N2, int KP, bool VEC, int RM = 16>
+// NORM: also the per-CTA partial sum of r^2 over the tile (npart[part_off + CTA index]; reduced in fixed order by
+// the caller) - the GMRES ||b|| fused into the first apply's Step (a) read of b
+template <int NT, int N2, int KP, bool VEC, int RM = 16, bool NORM = false>
 __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restrict__ r, long long S, long long p_begin,
                                                            long long npairs_chunk, double2* __restrict__ Y,
                                                            const double* __restrict__ gam,
                                                            const double2* __restrict__ tw2,
-                                                           const double2* __restrict__ twt) {
+                                                           const double2* __restrict__ twt,
+                                                           double* __restrict__ npart = nullptr,
+                                                           long long part_off = 0) {
   constexpr int N1 = NT / N2, C = KP, NTH = KP * N2 / RM;
   extern __shared__ double2 sm[];
   __shared__ double2 s_tw2[N2], s_twr[N2];  // 64-point twiddles; w_Nt^{t1 n2}, n2 < 64
@@ -31,6 +35,7 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restr
   }
   __syncthreads();
   const bool fullp = pl0 + KP <= Pc;
+  double nacc = 0.0;
   fft_io<N2, C, false, false, NTH, false, false, RM>(
       sm, s_tw2,
       [&](int j, auto st, int c, double2* v) {
@@ -54,6 +59,7 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restr
             if (okx) x = __ldcs(q + m * step);
             if (oky) y = __ldcs(q + m * step + 1);
           }
+          if (NORM) nacc = fma(x, x, fma(y, y, nacc));
           v[m] = make_double2(g * x, g * y);
         }
       },
@@ -64,6 +70,17 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restr
 #pragma unroll
         for (int m = 0; m < RL; ++m) __stcg(q + (long long)m * s * Pc, cmul(w[m], s_twr[j + m * s]));
       });
+  if constexpr (NORM) {  // fixed-order block reduction: warp trees, then warp 0 over the warp sums
+    __shared__ double s_red[32];
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = nacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NTH / 32; ++w) t += s_red[w];
+      npart[part_off + (long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
 
 // Forward stage 1 reading r = sum_k cb.c[k] cb.x[k] (pd_comb_args, 16-byte aligned vectors, S even): the

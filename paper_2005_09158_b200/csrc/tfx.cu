@@ -432,6 +432,7 @@ void set_attrs() {
   const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, true, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, false, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+  cudaFuncSetAttribute(tf4_fwd_s1<NT, N2, KP, true, kRS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tf4_fwd_s1_comb<NT, N2, KP, kRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
   cudaFuncSetAttribute(tfx_fwd_s2<NT, NX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   cudaFuncSetAttribute(tfx_inv_s1<NT, NX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -449,13 +450,15 @@ void set_attrs() {
 template <int NT, int NX>
 cudaError_t fwd(const double* r, const pd_spec& sp, long long S, const double* gam, const pd_tf4_tables& tb,
                 const double2* twx, double2* scratch0, long long chunk_pairs, cudaStream_t st0, int* nl,
-                const pd_tfx_overlap* ov, const pd_comb_args* comb) {
+                const pd_tfx_overlap* ov, const pd_comb_args* comb, double* npart, long long* nparts) {
   using F = Fx<NT, NX>;
   constexpr int N2 = F::N2, KP = F::KP, NP = F::NP;
   set_attrs<NT, NX>();
   const int sm1 = smem_of<N2>(KP), sm2 = F::SMEM * (int)sizeof(double2);
   const bool vec = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
-  const bool tma = !comb && pd_tf4_tma_supported(NT, S, r);
+  if (npart && (comb || !vec)) return cudaErrorInvalidValue;  // the norm rides on the 16-byte loader
+  long long poff = 0;
+  const bool tma = !comb && !npart && pd_tf4_tma_supported(NT, S, r);
   const long long npairs = S / 2;
   int n = 0;
   if (cudaError_t e = ov_fork(ov, st0)) return e;
@@ -469,6 +472,10 @@ cudaError_t fwd(const double* r, const pd_spec& sp, long long S, const double* g
       tf4_fwd_s1_comb<NT, N2, KP, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(*comb, S, p, pc, scratch, gam, tb.tw2, tb.twt);
     } else if (tma) {
       if (cudaError_t e = pd_launch_tf4_fwd_s1_tma(NT, r, S, p, pc, scratch, gam, tb.tw2, tb.twt, st)) return e;
+    } else if (npart) {
+      tf4_fwd_s1<NT, N2, KP, true, kRS, true><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt,
+                                                                            npart, poff);
+      poff += (long long)g1.x * g1.y;
     } else if (vec)
       tf4_fwd_s1<NT, N2, KP, true, kRS><<<g1, KP * N2 / kRS, sm1, st>>>(r, S, p, pc, scratch, gam, tb.tw2, tb.twt);
     else
@@ -484,6 +491,7 @@ cudaError_t fwd(const double* r, const pd_spec& sp, long long S, const double* g
     n += 2;
   }
   *nl = n;
+  if (nparts) *nparts = poff;
   return ov_join(ov, st0);
 }
 
@@ -565,8 +573,9 @@ long long pd_tfx_chunk_align(int nt, int nx) {
 
 cudaError_t pd_launch_tfx_fwd(int nt, int nx, const double* r, const pd_spec& sp, long long S, const double* gam,
                               const pd_tf4_tables& tb, const double2* twx, double2* scratch, long long chunk_pairs,
-                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov, const pd_comb_args* comb) {
-  PD_TFX_SWITCH(fwd, (r, sp, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov, comb))
+                              cudaStream_t st, int* nl, const pd_tfx_overlap* ov, const pd_comb_args* comb,
+                              double* npart, long long* nparts) {
+  PD_TFX_SWITCH(fwd, (r, sp, S, gam, tb, twx, scratch, chunk_pairs, st, nl, ov, comb, npart, nparts))
 }
 
 cudaError_t pd_launch_tfx_inv(int nt, int nx, const pd_spec& sp, double* z, long long S, const double* igam,

@@ -309,6 +309,30 @@ def test_gmres_final_assembly_variants_agree(monkeypatch, name):
         assert r1.iterations == rep_ref.iterations and rel(u1, u_ref) < SOLVE_TOL
 
 
+def test_gmres_fused_bnorm_matches_separate_dot(monkeypatch):
+    """Zero initial guess on the 2D four-step path: ||b|| taken by the first apply's Step (a) read of b (default) vs
+    a separate dot sweep (PD_GMRES_NO_FUSED_NORM=1): same iterations, solutions and residual within rounding (the
+    two sums differ only in association); b = 0 returns u = 0 with zero iterations in both."""
+    import torch
+    cfg = W.BY_NAME["cfg4"].scaled(nx=64, ny=64, nt=1024)
+    res = []
+    for env in (None, "1"):
+        monkeypatch.delenv("PD_GMRES_NO_FUSED_NORM", raising=False)
+        if env:
+            monkeypatch.setenv("PD_GMRES_NO_FUSED_NORM", env)
+        ctx = make_ctx(cfg)
+        b = ctx.build_rhs(to_dev(W.initial_u0(cfg)))
+        u, rep = ctx.solve_gmres(b, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit, zero_guess=True)
+        z = torch.zeros_like(b)
+        u0 = torch.full_like(b, float("nan"))
+        u0, rep0 = ctx.solve_gmres(z, u0, tol=cfg.tol, m=cfg.m, maxit=cfg.maxit, zero_guess=True)
+        assert rep0.converged and rep0.iterations == 0 and not bool(u0.abs().max() > 0)
+        res.append((to_host(u), rep))
+    (u1, r1), (u2, r2) = res
+    assert r1.converged and r1.iterations == r2.iterations
+    assert rel(u1, u2) < 1e-12 and abs(r1.rel_residual - r2.rel_residual) <= 1e-6 * r2.rel_residual
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg4s", "cfg3s"])
 def test_gmres_zero_guess_flag(name):
     """pd_solve(GMRES | PD_SOLVE_ZERO_GUESS) with u full of NaN (so any read of it would show) gives the same
