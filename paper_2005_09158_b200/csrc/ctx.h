@@ -115,6 +115,9 @@ struct pd_ctx {
   int* gm_flag = nullptr;        // zero-initial-guess check
   double* ivp_init = nullptr;    // pd_solve_ivp_host: u0, v0 on the device
   double* ivp_f = nullptr;       // pd_solve_ivp_host: source samples
+  double* ivp_dst = nullptr;     // pd_solve_ivp_host (GMRES): host destination of u, streamed behind the assembly
+  bool ivp_done = false;         // that copy was issued for the final u
+  cudaStream_t d2h_st = nullptr; // its copy stream
   int* gm_hflag = nullptr;
   // host-buffer staging
   double* stage_a = nullptr;

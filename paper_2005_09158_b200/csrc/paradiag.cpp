@@ -221,6 +221,7 @@ static void free_ctx(pd_ctx* c) {
   if (c->gm_head) cudaFree(c->gm_head);
   if (c->gm_full) cudaFree(c->gm_full);
   if (c->npart) cudaFree(c->npart);
+  if (c->d2h_st) cudaStreamDestroy(c->d2h_st);
   for (double* p : c->Zs) cudaFree(p);
   if (c->gm_flag) cudaFree(c->gm_flag);
   if (c->ivp_init) cudaFree(c->ivp_init);
@@ -1289,10 +1290,35 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     }
     for (int i = 0; i < kk; ++i) coef[i] = y[i] * sc[i];
     const int acc0 = u_is_zero ? 0 : 1;
+    bool streamed = false;  // u's D2H (pd_solve_ivp_host) already issued chunk by chunk behind the assembly
     if (useZ) {  // u (+)= sum_i coef_i Z_i: one sweep over kk + 1 vectors instead of an apply
       u_is_zero = false;
       std::vector<const double*> Zp(c->Zs.begin(), c->Zs.begin() + kk);
-      if (acc0 == 0) {
+      // pd_solve_ivp_host with a converged Arnoldi estimate: assemble u in row chunks and copy each chunk to the
+      // host on a second stream right behind it, so the host-link transfer overlaps the rest of the assembly and
+      // the true-residual check (the copy is waited for, and redone after the next cycle, if a restart follows)
+      const bool stream_d2h = c->ivp_dst && acc0 == 0 && std::fabs(gv[kk]) <= tol * bnorm;
+      if (stream_d2h) {
+        if (!c->d2h_st) PD_CUDA(c, cudaStreamCreateWithFlags(&c->d2h_st, cudaStreamNonBlocking));
+        const int K = 8;
+        long long rows = (c->nt + K - 1) / K;
+        if (rows % 2) ++rows;  // chunk starts 16-byte aligned for any S
+        for (long long r0 = 0; r0 < c->nt; r0 += rows) {
+          const long long nr = std::min<long long>(rows, c->nt - r0), off = r0 * c->S;
+          std::vector<const double*> Zc(kk);
+          for (int i = 0; i < kk; ++i) Zc[i] = Zp[i] + off;
+          s = pd_krylov_n(c, 3, Zc.data(), coef.data(), kk, 0.0, u + off, nr * c->S, nullptr);
+          if (s != PD_OK) return s;
+          cudaEvent_t ev;
+          PD_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          PD_CUDA(c, cudaEventRecord(ev, c->st));
+          PD_CUDA(c, cudaStreamWaitEvent(c->d2h_st, ev, 0));
+          PD_CUDA(c, cudaEventDestroy(ev));  // released once the wait has been satisfied
+          PD_CUDA(c, cudaMemcpyAsync(c->ivp_dst + off, u + off, sizeof(double) * nr * c->S, cudaMemcpyDeviceToHost,
+                                     c->d2h_st));
+        }
+        streamed = true;
+      } else if (acc0 == 0) {
         s = krylov_impl(c, 3, Zp.data(), coef.data(), kk, 0.0, u, nullptr);
       } else {
         double unused = 0;
@@ -1331,6 +1357,13 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
     if (norm_only && !(std::sqrt(rr) <= tol * bnorm) && its < maxit && !breakdown) {
       s = pd_stencil_impl(c, b, u, c->V[0], &rr);
       if (s != PD_OK) return s;
+    }
+    if (streamed) {
+      if (std::sqrt(rr) <= tol * bnorm || its >= maxit || breakdown) {
+        c->ivp_done = true;  // this u is final: its copy is in flight (pd_solve_ivp_host synchronises)
+      } else {
+        PD_CUDA(c, cudaStreamSynchronize(c->d2h_st));  // a restart rewrites u: finish the stale copy first
+      }
     }
     Xv[0] = c->V[0];
     beta = std::sqrt(rr);
@@ -1401,8 +1434,11 @@ pd_status pd_solve_host(pd_ctx* c, int solver, const double* bh, double* uh, dou
     PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
   s = solver == 0 ? pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep)
                   : gmres_impl(c, c->stage_a, c->stage_b, tol, m, maxit, rep, zero);
+  c->ivp_dst = nullptr;
+  if (c->d2h_st) PD_CUDA(c, cudaStreamSynchronize(c->d2h_st));
   if (s < 0) return s;
-  PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  if (!c->ivp_done) PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  c->ivp_done = false;
   PD_CUDA(c, cudaStreamSynchronize(c->st));
   return s;
 }
@@ -1428,6 +1464,8 @@ pd_status pd_solve_ivp_host(pd_ctx* c, int solver, const double* u0h, const doub
   if (s != PD_OK) return s;
   // from u = 0: GMRES takes the zero-guess path (u output only), the others start from a zeroed u
   if (solver != 1) PD_CUDA(c, cudaMemsetAsync(c->stage_b, 0, bytes, c->st));
+  c->ivp_dst = solver == 1 ? uh : nullptr;  // GMRES streams u to the host behind its final assembly
+  c->ivp_done = false;
   switch (solver) {
     case 0: s = pd_solve_stationary(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
     case 1: s = gmres_impl(c, c->stage_a, c->stage_b, tol, m, maxit, rep, true); break;
@@ -1435,8 +1473,11 @@ pd_status pd_solve_ivp_host(pd_ctx* c, int solver, const double* u0h, const doub
     case 3: s = pd_solve_gmres_tail(c, c->stage_a, c->stage_b, tol, m, maxit, rep); break;
     default: s = pd_solve_newton(c, c->stage_a, c->stage_b, tol, maxit, rep); break;
   }
+  c->ivp_dst = nullptr;
+  if (c->d2h_st) PD_CUDA(c, cudaStreamSynchronize(c->d2h_st));
   if (s < 0) return s;
-  PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  if (!c->ivp_done) PD_CUDA(c, cudaMemcpyAsync(uh, c->stage_b, bytes, cudaMemcpyDeviceToHost, c->st));
+  c->ivp_done = false;
   PD_CUDA(c, cudaStreamSynchronize(c->st));
   return s;
 }
