@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ctx.h"
 
 typedef std::complex<long double> cld;
@@ -687,7 +689,12 @@ pd_status pd_phase_times(pd_ctx* c, double* ms4, long long* n4) {
 
 // ---- phase timing: CUDA events recorded on the context stream around each kernel, resolved lazily
 // (pd_phase_times) so the timed region is not serialised by host syncs ----
+// NVTX ranges per kernel slot (nsys / ncu --nvtx timelines; a no-op without a tool attached)
+static const char* const kPhaseName[8] = {"step_a_time_fft",  "step_b_spatial_solve", "step_c_inverse_time_fft",
+                                          "residual",         "step_c_fused_update",  "matvec",
+                                          "krylov_sweep",     "residual_norm"};
 static void phase_begin(pd_ctx* c, int ph) {
+  nvtxRangePushA(kPhaseName[ph]);
   if (!c->timing) return;
   const int need = (int)(c->evrec.size() + 1) * 2;
   while ((int)c->evpool.size() < need) {
@@ -700,6 +707,7 @@ static void phase_begin(pd_ctx* c, int ph) {
   c->ev_open[ph] = i;
 }
 static void phase_end(pd_ctx* c, int ph) {
+  nvtxRangePop();
   if (!c->timing || c->ev_open[ph] < 0) return;
   const int i = c->ev_open[ph];
   cudaEventRecord(c->evpool[i + 1], c->st);

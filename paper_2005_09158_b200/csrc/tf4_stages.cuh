@@ -198,6 +198,19 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
           }
           return;
         } else if constexpr (!VEC && MODE) {
+          const bool a16 = oky && (reinterpret_cast<uintptr_t>(q) & 15) == 0;  // odd S, even t1 S: aligned rows
+          if (a16) {
+            double2 o[RL];
+#pragma unroll
+            for (int m = 0; m < RL; ++m) o[m] = __ldcs(reinterpret_cast<const double2*>(q + m * step));
+#pragma unroll
+            for (int m = 0; m < RL; ++m) {
+              const double g = s_g[j + m * s];
+              __stcs(reinterpret_cast<double2*>(q + m * step),
+                     make_double2(fma(g, w[m].x, o[m].x), fma(g, w[m].y, o[m].y)));
+            }
+            return;
+          }
           double ox[RL], oy[RL];
 #pragma unroll
           for (int m = 0; m < RL; ++m) {
@@ -212,11 +225,12 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
           }
           return;
         } else {
+          const bool a16 = VEC || (oky && (reinterpret_cast<uintptr_t>(q) & 15) == 0);
 #pragma unroll
           for (int m = 0; m < RL; ++m) {
             const double g = s_g[j + m * s];
             double* row = q + m * step;
-            if (VEC) {
+            if (a16) {
               __stcs(reinterpret_cast<double2*>(row), make_double2(g * w[m].x, g * w[m].y));
             } else {
               if (okx) row[0] = g * w[m].x;
