@@ -9,6 +9,8 @@
 // (1) row FFTs along x (rows are contiguous), (2) column FFT along y + divide + column IFFT (8 adjacent
 // columns per CTA = 128 B row segments), (3) row IFFTs along x.  When the time FFTs already did the x
 // transforms (tfx.cu, the default where supported) only launch (2) runs (cols_only).
+#include <cstdlib>
+
 #include "fft.cuh"
 #include "kernels.h"
 
@@ -623,6 +625,95 @@ dtri_kernel(double2* __restrict__ Sh, int slab0, int fglob0, const pd_dtri_coef*
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// DST-I rows by a HALF-length complex FFT (r02y; replaces the length-2(N+1) odd-extension FFT of dst_rows_kernel in
+// the dtri path).  For a row z_1..z_N (N1 = N + 1 a power of two, z_0 = z_N1 = 0) and s_j = sin(pi j / N1):
+//   y_j = s_j (z_j + z_{N1-j}) + (z_j - z_{N1-j}) / 2,   W = FFT_N1(y)     (complex-linear in z, so complex rows work)
+//   F_{2k}   = (i/2) (W_k - W_{N1-k})                        k = 1 .. N1/2 - 1
+//   F_{2k+1} = W_0 / 2 + sum_{i=1..k} (W_i + W_{N1-i}) / 2   k = 0 .. N1/2 - 1   (running sum: one warp scan per row)
+// give F_k = sum_j z_j sin(pi j k / N1) (the symmetric part of y transforms to F_{2k+1} - F_{2k-1}, the antisymmetric
+// part to F_{2k}).  The transform is its own inverse up to N1/2, so one kernel serves both directions and the y-pass
+// between them scales by 2/N1.  Half the FFT length, half the shared memory (two CTAs per SM at N1 = 512 instead of
+// one), the mirror loads hit L1.  Rounding: the running sum carries ~N1/2 additions (4e-14 of max|F| at N1 = 512).
+template <int N1>
+struct DsthCfg {
+  static constexpr int C = N1 >= 128 ? kBatch : 1024 / N1;  // rows per CTA (whole warps for the short rows)
+  static constexpr int NTH = C * N1 / 16;
+  static constexpr int MINB = NTH <= 128 ? 4 : 2;
+};
+
+template <int N1>
+__global__ void __launch_bounds__(DsthCfg<N1>::NTH, DsthCfg<N1>::MINB)
+dsth_rows_kernel(double2* __restrict__ base, long long nrows, const double2* __restrict__ twM) {
+  using T = DsthCfg<N1>;
+  constexpr int C = T::C, NTH = T::NTH, N = N1 - 1, R0 = first_radix(N1), RL = last_radix(N1);
+  extern __shared__ double2 sm[];
+  __shared__ double2 s_tw[N1];          // w_N1^k = twM[2k] (twM: the 2 N1-point table)
+  __shared__ double s_sin[N1 / 2 + 1];  // sin(pi j / N1) = -Im twM[j]
+  const long long row0 = (long long)blockIdx.x * C;
+  for (int i = threadIdx.x; i < N1; i += NTH) s_tw[i] = __ldg(twM + 2 * i);
+  for (int i = threadIdx.x; i <= N1 / 2; i += NTH) s_sin[i] = -__ldg(twM + i).y;
+  __syncthreads();
+  fft_io<N1, C, false, true, NTH, false, true>(
+      sm, s_tw,
+      [&](int j, auto st, int c, double2* v) {
+        constexpr int s = decltype(st)::value;
+        const bool ok = row0 + c < nrows;
+        const double2* q = base + (row0 + c) * N - 1;  // q[p] = z_p, p = 1..N
+#pragma unroll
+        for (int m = 0; m < R0; ++m) {
+          const int p = j + m * s;
+          if (ok && p != 0) {
+            const double2 a = __ldg(q + p), b = __ldg(q + N1 - p);
+            const double sj = s_sin[p <= N1 / 2 ? p : N1 - p];
+            v[m] = make_double2(fma(sj, a.x + b.x, 0.5 * (a.x - b.x)), fma(sj, a.y + b.y, 0.5 * (a.y - b.y)));
+          } else {
+            v[m] = czero();
+          }
+        }
+      },
+      [&](int j, auto st, int c, const double2* w) {
+        constexpr int s = decltype(st)::value;
+#pragma unroll
+        for (int m = 0; m < RL; ++m) sm[pad(c * N1 + j + m * s)] = w[m];
+      });
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int KB = (N1 / 2 + 31) / 32;
+  for (int c = warp; c < C; c += NTH / 32) {
+    if (row0 + c >= nrows) continue;  // warp-uniform
+    double2* q = base + (row0 + c) * N - 1;  // q[m] = F_m
+    double2 carry = czero();
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const int k = lane + 32 * i;
+      const bool act = k < N1 / 2;
+      double2 D = czero(), Fe = czero();
+      if (act) {
+        const double2 Wk = sm[pad(c * N1 + k)], Wm = sm[pad(c * N1 + ((N1 - k) & (N1 - 1)))];
+        D = k == 0 ? cscale(Wk, 0.5) : make_double2(0.5 * (Wk.x + Wm.x), 0.5 * (Wk.y + Wm.y));
+        Fe = make_double2(-0.5 * (Wk.y - Wm.y), 0.5 * (Wk.x - Wm.x));
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double tx = __shfl_up_sync(0xffffffffu, D.x, o), ty = __shfl_up_sync(0xffffffffu, D.y, o);
+        if (lane >= o) D = make_double2(D.x + tx, D.y + ty);
+      }
+      D = cadd(D, carry);
+      carry = make_double2(__shfl_sync(0xffffffffu, D.x, 31), __shfl_sync(0xffffffffu, D.y, 31));
+      if (act) {
+        if (k >= 1) __stcg(q + 2 * k, Fe);
+        __stcg(q + 2 * k + 1, D);
+      }
+    }
+  }
+}
+
+template <int N1>
+int smem_dsth() {
+  return smem_elems(DsthCfg<N1>::C * N1) * (int)sizeof(double2);
+}
+
 template <int M>
 cudaError_t dst_dtri_n(double2* Sh, int nfreq, int f0g, const pd_dtri_coef* coef, const double2* tw, int chunk,
                        cudaStream_t st, int* launches) {
@@ -639,15 +730,43 @@ cudaError_t dst_dtri_n(double2* Sh, int nfreq, int f0g, const pd_dtri_coef* coef
     if (e != cudaSuccess) return e;
     attr = dev_;
   }
+  // PD_DST_FULL=1: the length-M odd-extension FFT rows (the r02j path, kept for A/B and as a second implementation
+  // in the tests); PD_DST_CHUNK_MB: slabs per launch triple (default 0 = the caller's ~1 GB chunks: L2-sized chunks,
+  // whose three kernels run back to back on L2-resident slabs, measured slower - 16 / 32 / 64 / 128 MB: 3.32 / 2.97 /
+  // 2.48 / 2.38 ms vs 2.27 ms per T4A L = 512 Step (b), profiles/r02y_t4a_phases.txt: sub-wave grids)
+  const char* ef = getenv("PD_DST_FULL");
+  const char* ec = getenv("PD_DST_CHUNK_MB");
+  const bool full = ef && atoi(ef) != 0;
+  const long long chunk_mb = ec ? atoll(ec) : 0;
+  if (!full && chunk_mb > 0) {
+    long long cs = (chunk_mb << 20) / ((long long)N * N * (long long)sizeof(double2));
+    if (cs < 1) cs = 1;
+    if (cs < chunk) chunk = (int)cs;
+  }
+  using H = DsthCfg<N1>;
+  const int smh = smem_dsth<N1>();
+  static int attrh = -1;
+  if (attrh != dev_) {
+    cudaError_t e = cudaFuncSetAttribute(dsth_rows_kernel<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smh);
+    if (e != cudaSuccess) return e;
+    attrh = dev_;
+  }
   int nl = 0;
   for (int s0 = 0; s0 < nfreq; s0 += chunk) {
     const int ns = nfreq - s0 < chunk ? nfreq - s0 : chunk;
     double2* base = Sh + (long long)s0 * N * N;
     const long long nrows = (long long)ns * N;
-    const unsigned row_ctas = (unsigned)((nrows + T::C - 1) / T::C);
-    dst_rows_kernel<M, false><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
-    dtri_kernel<N1><<<dim3((N + kYC - 1) / kYC, ns), 32 * kYC, smd, st>>>(Sh, s0, f0g + s0, coef, 1.0 / M);
-    dst_rows_kernel<M, true><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+    if (full) {
+      const unsigned row_ctas = (unsigned)((nrows + T::C - 1) / T::C);
+      dst_rows_kernel<M, false><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+      dtri_kernel<N1><<<dim3((N + kYC - 1) / kYC, ns), 32 * kYC, smd, st>>>(Sh, s0, f0g + s0, coef, 1.0 / M);
+      dst_rows_kernel<M, true><<<row_ctas, T::NTH, smr, st>>>(base, nrows, tw);
+    } else {
+      const unsigned row_ctas = (unsigned)((nrows + H::C - 1) / H::C);
+      dsth_rows_kernel<N1><<<row_ctas, H::NTH, smh, st>>>(base, nrows, tw);
+      dtri_kernel<N1><<<dim3((N + kYC - 1) / kYC, ns), 32 * kYC, smd, st>>>(Sh, s0, f0g + s0, coef, 2.0 / N1);
+      dsth_rows_kernel<N1><<<row_ctas, H::NTH, smh, st>>>(base, nrows, tw);
+    }
     nl += 3;
   }
   if (launches) *launches = nl;

@@ -86,6 +86,20 @@ def test_apply_2d_dirichlet_dst_column_pass_matches_oracle(monkeypatch, op, sche
     check_apply(cfg, r, z)
 
 
+@pytest.mark.parametrize("env", [{"PD_DST_FULL": "1"}, {"PD_DST_CHUNK_MB": "1"}, {"PD_DST_CHUNK_MB": "0"}])
+@pytest.mark.parametrize("op,scheme,nx,nt", [(W.WAVE2D, W.LF, 31, 64), (W.WAVE2D, W.LF, 255, 16),
+                                             (W.WAVE2D, W.BE, 63, 8)])
+def test_apply_2d_dirichlet_dst_row_variants_match_oracle(monkeypatch, env, op, scheme, nx, nt):
+    """The x-DST rows of the 2D Dirichlet Step (b): the length-2(N+1) odd-extension FFT (PD_DST_FULL=1) instead of the
+    default half-length FFT, and the default with one-slab / whole-spectrum launch chunks (env read per call)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = _cfg(op, scheme, nx, nt, alpha=0.02)
+    r = W.random_vector(cfg, seed=nx + nt + 1)
+    z = to_host(make_ctx(cfg).apply_precond(to_dev(r)))
+    check_apply(cfg, r, z)
+
+
 @pytest.mark.parametrize("kov,mb", [(1, 1024), (1, 8), (2, 8), (4, 4)])
 @pytest.mark.parametrize("op,scheme,nx,nt", [(W.ADE2D, W.CN, 64, 1024), (W.ADE1D, W.BE, 2047, 4096)])
 def test_apply_time_fft_pipeline_variants(monkeypatch, op, scheme, nx, nt, kov, mb):
