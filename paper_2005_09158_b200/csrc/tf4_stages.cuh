@@ -12,20 +12,20 @@ using namespace pdfft;
 // ---------------------------------------------------------------------------------------------
 // NORM: also the per-CTA partial sum of r^2 over the tile (npart[part_off + CTA index]; reduced in fixed order by
 // the caller) - the GMRES ||b|| fused into the first apply's Step (a) read of b
-template <int NT, int N2, int KP, bool VEC, int RM = 16, bool NORM = false>
-__global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restrict__ r, long long S, long long p_begin,
-                                                           long long npairs_chunk, double2* __restrict__ Y,
-                                                           const double* __restrict__ gam,
-                                                           const double2* __restrict__ tw2,
-                                                           const double2* __restrict__ twt,
-                                                           double* __restrict__ npart = nullptr,
-                                                           long long part_off = 0) {
+// tile (bx, by) of the grid ((pairs + KP - 1) / KP, N1); ntx = tiles per t1 (the NORM partial index); a __device__
+// body so that the persistent fused kernel (tfx.cu) can run tiles of both stages from one task loop
+// PRE() runs in every thread right before its global stores (the persistent kernel's deferred task signal)
+template <int NT, int N2, int KP, bool VEC, int RM = 16, bool NORM = false, class PRE = NoHook>
+PD_D void tf4_fwd_s1_tile(const double* __restrict__ r, long long S, long long p_begin, long long npairs_chunk,
+                          double2* __restrict__ Y, const double* __restrict__ gam, const double2* __restrict__ tw2,
+                          const double2* __restrict__ twt, double* __restrict__ npart, long long part_off, int bx, int by,
+                          int ntx, PRE pre = PRE()) {
   constexpr int N1 = NT / N2, C = KP, NTH = KP * N2 / RM;
   extern __shared__ double2 sm[];
   __shared__ double2 s_tw2[N2], s_twr[N2];  // 64-point twiddles; w_Nt^{t1 n2}, n2 < 64
   __shared__ double s_g[N2];                 // Gamma of rows t1 + N1 t2
-  const int t1 = blockIdx.y;
-  const long long pl0 = (long long)blockIdx.x * KP;  // pair index within the chunk
+  const int t1 = by;
+  const long long pl0 = (long long)bx * KP;  // pair index within the chunk
   const long long p0 = p_begin + pl0;                // global pair index
   const long long Pc = npairs_chunk;
   for (int i = threadIdx.x; i < N2; i += NTH) {
@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restr
       },
       [&](int j, auto st, int c, const double2* w) {
         constexpr int s = decltype(st)::value, RL = last_radix(N2, RM);
+        pre();
         if (!(fullp || pl0 + c < Pc)) return;
         double2* q = Y + ((long long)t1 * N2 + j) * Pc + pl0 + c;
 #pragma unroll
@@ -78,9 +79,21 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restr
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < NTH / 32; ++w) t += s_red[w];
-      npart[part_off + (long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
+      npart[part_off + (long long)by * ntx + bx] = t;
     }
   }
+}
+
+template <int NT, int N2, int KP, bool VEC, int RM = 16, bool NORM = false>
+__global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1(const double* __restrict__ r, long long S, long long p_begin,
+                                                           long long npairs_chunk, double2* __restrict__ Y,
+                                                           const double* __restrict__ gam,
+                                                           const double2* __restrict__ tw2,
+                                                           const double2* __restrict__ twt,
+                                                           double* __restrict__ npart = nullptr,
+                                                           long long part_off = 0) {
+  tf4_fwd_s1_tile<NT, N2, KP, VEC, RM, NORM>(r, S, p_begin, npairs_chunk, Y, gam, tw2, twt, npart, part_off, blockIdx.x,
+                                             blockIdx.y, gridDim.x);
 }
 
 // Forward stage 1 reading r = sum_k cb.c[k] cb.x[k] (pd_comb_args, 16-byte aligned vectors, S even): the
@@ -147,18 +160,17 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_fwd_s1_comb(const __grid_con
 // inverse stage 2: for fixed t1 (blockIdx.y): N2-point inverse FFT over n2 of W[n2][t1][.], outputs
 // t = t1 + N1 t2 scaled by Gamma^{-1}_t / Nt into the two real columns of each pair (MODE 1: +=).
 // ---------------------------------------------------------------------------------------------
-template <int NT, int N2, int KP, bool VEC, int MODE, int RM = 16>
-__global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __restrict__ W, long long S, long long p_begin,
-                                                           long long npairs_chunk, double* __restrict__ z,
-                                                           const double* __restrict__ igam,
-                                                           const double2* __restrict__ tw2) {
+template <int NT, int N2, int KP, bool VEC, int MODE, int RM = 16, class PRE = NoHook>
+PD_D void tf4_inv_s2_tile(const double2* __restrict__ W, long long S, long long p_begin, long long npairs_chunk,
+                          double* __restrict__ z, const double* __restrict__ igam, const double2* __restrict__ tw2, int bx,
+                          int by, PRE pre = PRE()) {
   constexpr int N1 = NT / N2, C = KP, NTH = KP * N2 / RM;
   static_assert(num_passes(N2, RM) >= 2, "the hook-filled tables need pass 0's barrier");
   extern __shared__ double2 sm[];
   __shared__ double2 s_tw2[N2];
   __shared__ double s_g[N2];  // Gamma^{-1} / Nt of rows t1 + N1 t2
-  const int t1 = blockIdx.y;
-  const long long pl0 = (long long)blockIdx.x * KP;
+  const int t1 = by;
+  const long long pl0 = (long long)bx * KP;
   const long long p0 = p_begin + pl0;
   const long long Pc = npairs_chunk;
   auto tables = [&] {  // first read behind pass 0's barrier (twiddles) and in the storer (Gamma)
@@ -179,6 +191,7 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
       },
       [&](int j, auto st, int c, const double2* w) {
         constexpr int s = decltype(st)::value, RL = last_radix(N2, RM);
+        pre();
         if (!(fullp || pl0 + c < Pc)) return;
         const long long col = 2 * (p0 + c);
         double* q = z + (long long)(t1 + N1 * j) * S + col;
@@ -240,6 +253,14 @@ __global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __rest
         }
       },
       tables);
+}
+
+template <int NT, int N2, int KP, bool VEC, int MODE, int RM = 16>
+__global__ void __launch_bounds__(KP * N2 / RM) tf4_inv_s2(const double2* __restrict__ W, long long S, long long p_begin,
+                                                           long long npairs_chunk, double* __restrict__ z,
+                                                           const double* __restrict__ igam,
+                                                           const double2* __restrict__ tw2) {
+  tf4_inv_s2_tile<NT, N2, KP, VEC, MODE, RM>(W, S, p_begin, npairs_chunk, z, igam, tw2, blockIdx.x, blockIdx.y);
 }
 
 template <int N>

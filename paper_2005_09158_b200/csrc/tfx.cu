@@ -254,17 +254,15 @@ PD_D void untangle_store(double2* out, int i, double2 x, double2 y, double2 w) {
   __stcs(out + i + NP, csub(E, wO));
 }
 
-template <int NT, int NX, bool SH>
-__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(const double2* __restrict__ Y, long long S,
-                                                              long long p_begin, long long Pc,
-                                                              const pd_spec sp,
-                                                              const double2* __restrict__ twx) {
+template <int NT, int NX, bool SH, class PRE = NoHook>
+PD_D void tfx_fwd_s2x_tile(const double2* __restrict__ Y, long long S, long long p_begin, long long Pc, const pd_spec& sp,
+                           const double2* __restrict__ twx, int bx, int by, PRE pre = PRE()) {
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
   extern __shared__ double2 sm[];
   __shared__ double2 s_twx[NP], s_tws[NP - 1];
-  const int n2 = blockIdx.y, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
-  const long long pl0 = (long long)blockIdx.x * NP;
+  const int n2 = by, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
+  const long long pl0 = (long long)bx * NP;
   const long long p0 = p_begin + pl0;
   // (1) NP-point FFTs over p of the 2 N1 rows c = (set, t1) straight from Y[t1][n2][pair]; the twiddle
   // tables are filled by the hook, after the tile loads are in flight (first used behind pass 0's barrier)
@@ -288,6 +286,7 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(cons
       },
       tables);
   __syncthreads();
+  pre();
   // (2) N1-point DFTs over t1 of column k (set 0) and column NP - k (partner set), untangle, store
   const int sb = nsets == 2 ? 1 : 0;
   for (int k = threadIdx.x; k < NP; k += NTH) {
@@ -319,6 +318,14 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(cons
   }
 }
 
+template <int NT, int NX, bool SH>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_fwd_s2x(const double2* __restrict__ Y, long long S,
+                                                              long long p_begin, long long Pc,
+                                                              const pd_spec sp,
+                                                              const double2* __restrict__ twx) {
+  tfx_fwd_s2x_tile<NT, NX, SH>(Y, S, p_begin, Pc, sp, twx, blockIdx.x, blockIdx.y);
+}
+
 // A_n[i] = E + iO from X_n[i], X_n[i + NP]:  E = x0 + x1, O = (x0 - x1) w^-i;  the mirror row
 // A_{Nt-n}[-i] = conj(E - iO)
 PD_D double2 a_direct(double2 x0, double2 x1, double2 wi) {
@@ -330,21 +337,19 @@ PD_D double2 a_mirror(double2 x0, double2 x1, double2 wi) {
   return make_double2(E.x + O.y, O.x - E.y);
 }
 
-template <int NT, int NX, bool SH>
-__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(const pd_spec sp, long long S,
-                                                              long long p_begin, long long Pc,
-                                                              double2* __restrict__ W,
-                                                              const double2* __restrict__ twx,
-                                                              const double2* __restrict__ twt) {
+template <int NT, int NX, bool SH, class PRE = NoHook>
+PD_D void tfx_inv_s1x_tile(const pd_spec& sp, long long S, long long p_begin, long long Pc, double2* __restrict__ W,
+                           const double2* __restrict__ twx, const double2* __restrict__ twt, int bx, int by,
+                           PRE pre = PRE()) {
   using F = Fx<NT, NX>;
   constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, NTH = F::NTH;
   constexpr int NV = N1 / 2 + 1;  // rows n = r + N2 n1 <= Nt/2 have n1 <= N1/2
   static_assert(NTH >= NP, "phase (0) runs one index k per thread");
   extern __shared__ double2 sm[];
   __shared__ double2 s_tws[NP - 1], s_twa[N1], s_twb[N1];
-  const int n2 = blockIdx.y, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
+  const int n2 = by, n2p = (N2 - n2) % N2, nsets = n2p == n2 ? 1 : 2;
   const int rb = nsets == 2 ? n2p : n2;  // residue of the partner set (self-partnered: the same set)
-  const long long pl0 = (long long)blockIdx.x * NP;
+  const long long pl0 = (long long)bx * NP;
   const long long p0 = p_begin + pl0;
   if (threadIdx.x < N1) {  // read behind the barrier that ends phase (0)
     s_twa[threadIdx.x] = cconj(__ldg(twt + threadIdx.x * n2));
@@ -413,12 +418,189 @@ __global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(cons
       [&](int j, auto st, int c, const double2* w) {
         constexpr int s = decltype(st)::value, RL = last_radix(NP, kRX);
         const int set = c / N1, t1 = c % N1;
+        pre();
         if (set == 1 && nsets == 1) return;  // the partner set is the same residue
         const double2 tw = (set ? s_twb : s_twa)[t1];
         double2* q = W + ((long long)(set ? n2p : n2) * N1 + t1) * Pc + pl0 + j;
 #pragma unroll
         for (int m = 0; m < RL; ++m) __stcg(q + m * s, cmul(w[m], tw));
       });
+}
+
+template <int NT, int NX, bool SH>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB) tfx_inv_s1x(const pd_spec sp, long long S,
+                                                              long long p_begin, long long Pc,
+                                                              double2* __restrict__ W,
+                                                              const double2* __restrict__ twx,
+                                                              const double2* __restrict__ twt) {
+  tfx_inv_s1x_tile<NT, NX, SH>(sp, S, p_begin, Pc, W, twx, twt, blockIdx.x, blockIdx.y);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Persistent fused time FFT (PD_TFX_PERSIST=1, r02 experiment): ONE launch per call.  Resident CTAs pull tile tasks
+// of both stages from a global counter, in an order that keeps stage 2 a fixed lag of kLag x-rows behind stage 1:
+//   block k = [stage-1 tiles of x-row k][stage-2 tiles of x-row k - kLag]
+// so the stage-1 -> stage-2 scratch is a ring of kRing x-rows (kRing * Nt * NX/2 complex, L2-resident) instead of the
+// per-stream chunk buffers, and there are no kernel boundaries (no single-wave launches, no launch gaps).  A
+// stage-2 tile of row y waits for done1[y] = all stage-1 tiles of the row (thread 0 polls, then a CTA barrier); a
+// stage-1 tile of row y waits for done2[y - kRing] before it overwrites that ring slot.  Tasks are claimed in
+// increasing order and a task only ever waits for lower-numbered ones, which running CTAs own: no deadlock, whatever
+// the number of resident CTAs.  Tiles are the very device bodies of the per-chunk kernels.
+// deferred completion signal of the previous tile: thread 0 fences and bumps the flag right before the CURRENT
+// tile's stores, when the previous tile's stores (ordered before by the loop's CTA barriers) have long drained, so
+// the fence costs nothing; signalling right after a tile's stores would stall the CTA for their round trip
+struct TaskSignal {
+  int** pending;  // CTA-uniform, in shared memory
+  PD_D void operator()() const {
+    if (threadIdx.x == 0 && *pending) {
+      __threadfence();
+      atomicAdd(*pending, 1);
+      *pending = nullptr;
+    }
+  }
+};
+// wait until *flag reaches target (thread 0 polls, then a CTA barrier).  Before it blocks, the CTA releases its own
+// deferred signal: the tile it waits for may itself be waiting for that one
+PD_D void task_wait(const int* flag, int target, const TaskSignal& sig) {
+  if (threadIdx.x == 0) {
+    const volatile int* f = reinterpret_cast<const volatile int*>(flag);
+    if (*f < target) {
+      sig();
+      while (*f < target) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+// task t -> (kind 0 = first stage / 1 = second stage, x-row y, tile); NA / NB tiles per row of the two kinds
+PD_D void task_decode(int t, int rows, int lag, int NA, int NB, int& kind, int& y, int& tile) {
+  const int head = lag * NA, per = NA + NB;
+  if (t < head) {
+    kind = 0;
+    y = t / NA;
+    tile = t % NA;
+    return;
+  }
+  const int t1 = t - head, k = lag + t1 / per, rem = t1 % per;
+  if (k < rows) {
+    kind = rem < NA ? 0 : 1;
+    y = kind ? k - lag : k;
+    tile = kind ? rem - NA : rem;
+    return;
+  }
+  const int t2 = t - (head + (rows - lag) * per);
+  kind = 1;
+  y = rows - lag + t2 / NB;
+  tile = t2 % NB;
+}
+
+// FWD: stage 1 = tf4_fwd_s1 tiles, stage 2 = tfx_fwd_s2x tiles;  !FWD: stage 1 = tfx_inv_s1x, stage 2 = tf4_inv_s2
+template <int NT, int NX, bool FWD>
+__global__ void __launch_bounds__(Fx<NT, NX>::NTH, PD_TFX_MINB)
+tfx_persist(const double* __restrict__ r, double* __restrict__ z, long long S, int rows, int lag, int ring_rows,
+            double2* __restrict__ ring, const pd_spec sp, const double* __restrict__ gam,
+            const double2* __restrict__ tw2, const double2* __restrict__ twt, const double2* __restrict__ twx,
+            int* __restrict__ ctr) {
+  using F = Fx<NT, NX>;
+  constexpr int N1 = F::N1, N2 = F::N2, NP = F::NP, KP = F::KP, TX = NP / KP;
+  constexpr int NT1 = TX * N1, NT2 = N2 / 2 + 1;  // tiles per x-row: N2-point stage / x-FFT stage
+  constexpr int NA = FWD ? NT1 : NT2, NB = FWD ? NT2 : NT1;
+  static_assert(KP * N2 / kRS == F::NTH, "both tile kinds run on the same thread count");
+  __shared__ int s_task;
+  __shared__ int* s_pending;
+  int* done1 = ctr + 1;
+  int* done2 = ctr + 1 + rows;
+  const int total = rows * (NA + NB);
+  const TaskSignal sig{&s_pending};
+  int nxt = 0;
+  if (threadIdx.x == 0) {
+    s_pending = nullptr;
+    nxt = atomicAdd(ctr, 1);
+  }
+  for (;;) {
+    __syncthreads();  // the previous tile's shared-memory reads and global stores are issued
+    if (threadIdx.x == 0) s_task = nxt;
+    __syncthreads();
+    const int t = s_task;
+    if (t >= total) break;
+    if (threadIdx.x == 0) nxt = atomicAdd(ctr, 1);  // the next task, in flight behind this tile
+    int kind, y, tile;
+    task_decode(t, rows, lag, NA, NB, kind, y, tile);
+    double2* Y = ring + (size_t)(y % ring_rows) * NT * NP;
+    int* mine;
+    if (kind == 0) {
+      if (y >= ring_rows) task_wait(done2 + y - ring_rows, NB, sig);
+      if constexpr (FWD)
+        tf4_fwd_s1_tile<NT, N2, KP, true, kRS, false>(r, S, (long long)y * NP, NP, Y, gam, tw2, twt, nullptr, 0, tile % TX,
+                                                      tile / TX, TX, sig);
+      else
+        tfx_inv_s1x_tile<NT, NX, false>(sp, S, (long long)y * NP, NP, Y, twx, twt, 0, tile, sig);
+      mine = done1 + y;
+    } else {
+      task_wait(done1 + y, NA, sig);
+      if constexpr (FWD)
+        tfx_fwd_s2x_tile<NT, NX, false>(Y, S, (long long)y * NP, NP, sp, twx, 0, tile, sig);
+      else
+        tf4_inv_s2_tile<NT, N2, KP, true, 0, kRS>(Y, S, (long long)y * NP, NP, z, gam, tw2, tile % TX, tile / TX, sig);
+      mine = done2 + y;
+    }
+    if (threadIdx.x == 0) s_pending = mine;  // thread 0 passed its pre-store hook: the older signal is out
+  }
+  sig();  // s_task >= total: all threads are past the loop barrier; the last tile's stores precede it
+}
+
+// workspace of the persistent kernels (experiment: one per process and device, allocated on first use)
+struct PersistWs {
+  int dev = -1;
+  int* ctr = nullptr;
+  int nctr = 0;
+  double2* ring = nullptr;
+  size_t ring_elems = 0;
+};
+inline cudaError_t persist_ws(PersistWs& w, int nctr, size_t ring_elems) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (w.dev != dev || w.nctr < nctr || w.ring_elems < ring_elems) {
+    if (w.dev == dev) {
+      cudaFree(w.ctr);
+      cudaFree(w.ring);
+    }
+    w = PersistWs{};
+    if (cudaError_t e = cudaMalloc(&w.ctr, (size_t)nctr * sizeof(int))) return e;
+    if (cudaError_t e = cudaMalloc(&w.ring, ring_elems * sizeof(double2))) return e;
+    w.dev = dev;
+    w.nctr = nctr;
+    w.ring_elems = ring_elems;
+  }
+  return cudaSuccess;
+}
+// lag (x-rows between the stages) so that a stage-2 tile's inputs were claimed ~2.5 grids of tasks earlier, and the ring
+// that holds the rows in flight (lag + the rows being written + slack); PD_TFX_LAG overrides
+template <int NT, int NX>
+inline void persist_plan(int grid, int rows, int* lag, int* ring_rows) {
+  using F = Fx<NT, NX>;
+  const int per = (F::NP / F::KP) * F::N1 + F::N2 / 2 + 1;
+  const char* e = getenv("PD_TFX_LAG");
+  int l = e ? atoi(e) : (5 * grid / 2 + per - 1) / per;
+  if (l < 2) l = 2;
+  if (l > rows - 1) l = rows - 1;
+  *lag = l;
+  *ring_rows = l + 3 + (grid + per - 1) / per;
+}
+inline bool persist_enabled() {
+  const char* e = getenv("PD_TFX_PERSIST");
+  return e && atoi(e) != 0;
+}
+template <class K>
+inline cudaError_t persist_grid(K kernel, int nth, int smem, int* grid) {
+  int dev = 0, nsm = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) return e;
+  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nth, smem)) return e;
+  if (occ < 1) return cudaErrorLaunchOutOfResources;
+  *grid = nsm * occ;
+  return cudaSuccess;
 }
 
 template <int NT, int NX>
@@ -461,6 +643,23 @@ cudaError_t fwd(const double* r, const pd_spec& sp, long long S, const double* g
   const bool tma = !comb && !npart && pd_tf4_tma_supported(NT, S, r);
   const long long npairs = S / 2;
   int n = 0;
+  if constexpr (KP * N2 / kRS == F::NTH && NP % KP == 0) {
+    const long long rows = S / NX;
+    if (persist_enabled() && !comb && !npart && vec && sp.P == 1 && rows >= 16 && rows * NX == S && rows < (1 << 20)) {
+      static PersistWs ws;
+      const int nctr = 1 + 2 * (int)rows, smem = sm1 > sm2 ? sm1 : sm2;
+      int grid = 0, lag = 0, ring_rows = 0;
+      if (cudaError_t e = persist_grid(tfx_persist<NT, NX, true>, F::NTH, smem, &grid)) return e;
+      persist_plan<NT, NX>(grid, (int)rows, &lag, &ring_rows);
+      if (cudaError_t e = persist_ws(ws, nctr, (size_t)ring_rows * NT * NP)) return e;
+      if (cudaError_t e = cudaMemsetAsync(ws.ctr, 0, (size_t)nctr * sizeof(int), st0)) return e;
+      tfx_persist<NT, NX, true><<<grid, F::NTH, smem, st0>>>(r, nullptr, S, (int)rows, lag, ring_rows, ws.ring, sp, gam,
+                                                            tb.tw2, tb.twt, twx, ws.ctr);
+      *nl = 1;
+      if (nparts) *nparts = 0;
+      return cudaGetLastError();
+    }
+  }
   if (cudaError_t e = ov_fork(ov, st0)) return e;
   for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
     const int lane = ov ? (int)(ci % ov->k) : 0;
@@ -506,6 +705,22 @@ cudaError_t inv(const pd_spec& sp, double* z, long long S, const double* igam, c
   const bool vec = (reinterpret_cast<uintptr_t>(z) & 15) == 0;
   const long long npairs = S / 2;
   int n = 0;
+  if constexpr (KP * N2 / kRS == F::NTH && NP % KP == 0) {
+    const long long rows = S / NX;
+    if (persist_enabled() && !accumulate && vec && sp.P == 1 && rows >= 16 && rows * NX == S && rows < (1 << 20)) {
+      static PersistWs ws;
+      const int nctr = 1 + 2 * (int)rows, smem = sm1 > sm2 ? sm1 : sm2;
+      int grid = 0, lag = 0, ring_rows = 0;
+      if (cudaError_t e = persist_grid(tfx_persist<NT, NX, false>, F::NTH, smem, &grid)) return e;
+      persist_plan<NT, NX>(grid, (int)rows, &lag, &ring_rows);
+      if (cudaError_t e = persist_ws(ws, nctr, (size_t)ring_rows * NT * NP)) return e;
+      if (cudaError_t e = cudaMemsetAsync(ws.ctr, 0, (size_t)nctr * sizeof(int), st0)) return e;
+      tfx_persist<NT, NX, false><<<grid, F::NTH, smem, st0>>>(nullptr, z, S, (int)rows, lag, ring_rows, ws.ring, sp, igam,
+                                                             tb.tw2, tb.twt, twx, ws.ctr);
+      *nl = 1;
+      return cudaGetLastError();
+    }
+  }
   if (cudaError_t e = ov_fork(ov, st0)) return e;
   for (long long p = 0, ci = 0; p < npairs; p += chunk_pairs, ++ci) {
     const int lane = ov ? (int)(ci % ov->k) : 0;

@@ -161,6 +161,18 @@ def test_apply_full_config_vs_oracle(name):
     check_apply(cfg, r, z)
 
 
+@pytest.mark.parametrize("nt", [256, 512])
+def test_apply_persistent_fused_time_fft_matches_oracle(monkeypatch, nt):
+    """PD_TFX_PERSIST=1 (experiment): one persistent launch per time FFT whose CTAs pull the tiles of both
+    four-step stages from a task counter with per-x-row completion flags (256 x-rows: the ring wraps, both waits run).
+    Same tiles as the default chunk pipeline; oracle parity at the config-3 shape and at Nt = 512."""
+    monkeypatch.setenv("PD_TFX_PERSIST", "1")
+    cfg = W.BY_NAME["cfg3"].scaled(nt=nt)
+    r = W.random_vector(cfg, seed=nt)
+    z = to_host(make_ctx(cfg).apply_precond(to_dev(r)))
+    check_apply(cfg, r, z)
+
+
 def test_wave_apply_vs_extended_precision():
     """Reading t1 pinned from above: on the config-2 recipe at 1023 x 1024 the GPU apply is within the north_star
     1e-10 of an extended-precision reference (O2 modal in np.longdouble, pinned in the CPU suite), with both fp64
