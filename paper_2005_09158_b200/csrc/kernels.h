@@ -73,9 +73,10 @@ struct pd_tri_coef {
   double2 r2;    // characteristic root with |r2| <= |r1| of c r^2 + b r + a = 0  (= a tau)
   double2 s;     // 1/r1 (= c tau)
   double2 tau;   // 1/(c r1) = 2/(-b -+ sqrt(b^2 - 4ac)), larger-magnitude denominator
-  double2 c;     // super-diagonal c = lam2 * sup
   double2 r2L;   // r2^L (L = rows per thread)
   double2 sL;    // s^L
+  double2 k1;    // boundary correction x_i += x^(d)_0 (k1 r2^{i+1} + k2 s^{N-i}): c kappa / (1 - c q_0),
+  double2 k2;    //   kappa = -tau / (1 - s r2); k2 = -k1 r2^{N+1}
 };
 cudaError_t pd_launch_tridiag(double2* Sh, int nx, int nfreq, const pd_tri_coef* coef, int rows_per_thread,
                               cudaStream_t st);
@@ -158,9 +159,11 @@ int pd_slab2d_ytri_supported(int n);
 // M = 2(N+1) of the odd extension; mu[k] = (4 nu/h^2) sin^2(pi k/M), k < M; tw: M-point twiddles
 int pd_slab2d_dst_supported(int n);
 // 2D Dirichlet Step (b) as x-DST rows -> y Dirichlet Toeplitz solves per (n, kx) -> inverse x-DST rows (slab2d.cu
-// dtri): one table entry per (frequency, kx < N), the constants of pd_tri_coef plus g = 1/(1 - c q_0)
+// dtri): one table entry per (frequency, kx < N): the roots and their lane powers (L = (N+1)/32 rows per lane) and the
+// closed-form boundary correction x_i += x^(d)_0 (k1 r2^{i+1} + k2 s^{N-i}), k1 = c g kappa, k2 = -k1 r2^{N+1},
+// g = 1/(1 - c q_0), kappa = -tau/(1 - s r2)
 struct pd_dtri_coef {
-  double2 r2, s, tau, c, r2L, sL, g;
+  double2 r2, s, tau, r2L, sL, sLm1, k1, k2;
 };
 int pd_slab2d_dtri_supported(int n);
 cudaError_t pd_launch_slab2d_dtri(double2* Sh, int n, int nfreq, int f0_glob, const pd_dtri_coef* coef,

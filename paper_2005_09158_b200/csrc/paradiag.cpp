@@ -185,11 +185,16 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
     if (std::abs(piv) < 1e-12L)
       return fail(c, PD_ESINGULAR, "shifted system lambda1 I + lambda2 K singular at frequency n=%d (|1-c q0|=%.3Le)",
                   n, std::abs(piv));
+    // the closed-form boundary response divides by 1 - s r2 (= 1 - r2/r1: a double root leaves the regime)
+    const cld geo = 1.0L - s * r2;
+    if (std::abs(geo) < 1e-7L) {
+      c->use_gtsv = true;
+      break;
+    }
     pd_tri_coef t;
     t.r2 = d2(r2);
     t.s = d2(s);
     t.tau = d2(tau);
-    t.c = d2(Cc);
     cld r2L = 1.0L, sL = 1.0L;
     for (int j = 0; j < L; ++j) {
       r2L *= r2;
@@ -197,6 +202,11 @@ static pd_status tri_coefs(pd_ctx* c, const std::vector<cld>& l1, const std::vec
     }
     t.r2L = d2(r2L);
     t.sL = d2(sL);
+    cld r2N1 = r2;
+    for (int j = 0; j < N; ++j) r2N1 *= r2;
+    const cld k1 = Cc / piv * (-tau / geo);
+    t.k1 = d2(k1);
+    t.k2 = d2(-k1 * r2N1);
     out[n] = t;
   }
   if (c->use_gtsv) {
@@ -452,19 +462,22 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
             rpw *= r2;
           }
           q0 *= -tau;
-          const cld piv = 1.0L - Cc * q0;
-          if (std::abs(piv) < 1e-12L) {
+          const cld piv = 1.0L - Cc * q0, geo = 1.0L - sv * r2;
+          // the closed-form response q_i = kappa (r2^{i+1} - r2^{N+1} s^{N-i}) divides by 1 - s r2
+          if (std::abs(piv) < 1e-12L || std::abs(geo) < 1e-7L) {
             ok = false;
             break;
           }
+          const cld k1 = Cc / piv * (-tau / geo);
           pd_dtri_coef& t = dt[(size_t)n * N + kx];
           t.r2 = d2(r2);
           t.s = d2(sv);
           t.tau = d2(tau);
-          t.c = d2(Cc);
           t.r2L = d2(cp(r2, L));
           t.sL = d2(cp(sv, L));
-          t.g = d2(1.0L / piv);
+          t.sLm1 = d2(cp(sv, L - 1));
+          t.k1 = d2(k1);
+          t.k2 = d2(-k1 * cp(r2, N + 1));
         }
       if (ok) {
         SETUP_CUDA(dalloc(&c->dtri, dt.size()));

@@ -583,37 +583,39 @@ dtri_kernel(double2* __restrict__ Sh, int slab0, int fglob0, const pd_dtri_coef*
       d[j] = cfma(rp, vin, d[j]);
       rp = cmul(rp, cf.r2);
     }
-  // backward: x_i = s x_{i+1} - tau w_i (x_N = 0), and the response q to w_i = r2^{i+1} (same recurrence)
+  // backward: x_i = s x_{i+1} - tau w_i (x_N = 0)
   const double2 mtau = cneg(cf.tau);
-  const double2 B = cmul(mtau, cpow_small(cf.r2, i0 + 1));  // -tau r2^{i0+1}
-  double2 rq[L];  // -tau r2^{i+1} for the lane's rows
-  rq[0] = B;
-#pragma unroll
-  for (int j = 1; j < L; ++j) rq[j] = cmul(rq[j - 1], cf.r2);
   p = czero();
-  double2 pq = czero();
 #pragma unroll
   for (int j = L - 1; j >= 0; --j)
     if (j < Lk) {
       p = cfma(cf.s, p, cmul(mtau, d[j]));
       d[j] = p;
-      pq = cfma(cf.s, pq, rq[j]);
-      rq[j] = pq;
     }
   const double2 xin = warp_affine_scan<true>(p, cf.sL, &tot);
-  const double2 qin = warp_affine_scan<true>(pq, cf.sL, &tot);
+  // rank-1 boundary correction in closed form.  The response of the same backward recurrence to w_i = r2^{i+1} is
+  //   q_i = -tau sum_{k >= i} s^{k-i} r2^{k+1} = kappa (r2^{i+1} - r2^{N+1} s^{N-i}),  kappa = -tau / (1 - s r2),
+  // so x_i = x^(d)_i + (c g x^(d)_0) q_i = x^(d)_i + X0 (k1 r2^{i+1} + k2 s^{N-i}) with the host constants
+  // k1 = c g kappa, k2 = -k1 r2^{N+1}: the s-term joins the lane's carry from above (s^{N-i} = s^{N-top} s^{top-i}),
+  // the r2-term is one running product - no second recurrence, scan or 16-row table (r02ac)
+  const double2 X0 = shfl2(cfma(cf.sL, xin, d[0]), 0);  // x^(d)_0: lane 0 holds L full rows
+  const double2 G2 = cmul(cf.k2, X0);
+  // s^{N - (i0 + Lk)}: 1 on the last lane, s^{L-1} (s^L)^{30 - lane} below
+  const double2 stop = lane == 31 ? make_double2(1.0, 0.0) : cmul(cf.sLm1, cpow_small(cf.sL, 30 - lane));
+  const double2 xin2 = cfma(G2, stop, xin);
   double2 sp = make_double2(1.0, 0.0);  // s^{Lk - j}, built from the top row down
 #pragma unroll
   for (int j = L - 1; j >= 0; --j)
     if (j < Lk) {
       sp = cmul(sp, cf.s);
-      d[j] = cfma(sp, xin, d[j]);
-      rq[j] = cfma(sp, qin, rq[j]);
+      d[j] = cfma(sp, xin2, d[j]);
     }
-  // x_0 = x^(d)_0 / (1 - c q_0);  x_i += (c x_0) q_i
-  const double2 cx0 = cmul(cf.c, cmul(shfl2(d[0], 0), cf.g));
+  double2 rg = cmul(cmul(cf.k1, X0), cmul(cf.r2, cpow_small(cf.r2L, lane)));  // k1 X0 r2^{i0 + 1}
 #pragma unroll
-  for (int j = 0; j < L; ++j) d[j] = cscale(cfma(cx0, rq[j], d[j]), scale);
+  for (int j = 0; j < L; ++j) {
+    d[j] = cscale(cadd(d[j], rg), scale);
+    rg = cmul(rg, cf.r2);
+  }
 #pragma unroll
   for (int j = 0; j < L; ++j)
     if (j < Lk) col[j] = d[j];
@@ -648,14 +650,15 @@ dsth_rows_kernel(double2* __restrict__ base, long long nrows, const double2* __r
   using T = DsthCfg<N1>;
   constexpr int C = T::C, NTH = T::NTH, N = N1 - 1, R0 = first_radix(N1), RL = last_radix(N1);
   extern __shared__ double2 sm[];
-  __shared__ double2 s_tw[N1];          // w_N1^k = twM[2k] (twM: the 2 N1-point table)
+  __shared__ double2 s_tws[N1 - 1];     // Stockham-ordered w_N1^k = twM[2k] (twM: the 2 N1-point table): the plain
+                                        // table read at the strides m k of the second radix-16 pass is bank conflicted
   __shared__ double s_sin[N1 / 2 + 1];  // sin(pi j / N1) = -Im twM[j]
   const long long row0 = (long long)blockIdx.x * C;
-  for (int i = threadIdx.x; i < N1; i += NTH) s_tw[i] = __ldg(twM + 2 * i);
+  build_stockham_table<N1, 16>(s_tws, [&](int idx) { return __ldg(twM + 2 * idx); });
   for (int i = threadIdx.x; i <= N1 / 2; i += NTH) s_sin[i] = -__ldg(twM + i).y;
   __syncthreads();
   fft_io<N1, C, false, true, NTH, false, true>(
-      sm, s_tw,
+      sm, TwStockham{s_tws},
       [&](int j, auto st, int c, double2* v) {
         constexpr int s = decltype(st)::value;
         const bool ok = row0 + c < nrows;

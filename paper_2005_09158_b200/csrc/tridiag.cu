@@ -7,7 +7,7 @@
 // i.e. a stable forward first-order recurrence (|r2| < 1) followed by a stable backward one
 //   x_i = s x_{i+1} - tau w_i,  s = 1/r1, tau = 1/(c r1)   (|s| < 1),
 // plus one rank-1 correction for the unknown x_0:  x = x^(d) + (c x_0) q, x_0 = x^(d)_0 / (1 - c q_0), where q
-// is the response to w^(1)_i = r2^{i+1}.  tau = 2/(-b -+ sqrt(b^2-4ac)) stays finite when c -> 0 (lower
+// is the response to w^(1)_i = r2^{i+1}, a geometric sum with the closed form kappa (r2^{i+1} - r2^{N+1} s^{N-i}).  tau = 2/(-b -+ sqrt(b^2-4ac)) stays finite when c -> 0 (lower
 // bidiagonal limit) and r2 = a tau, s = c tau.  Setup checks |r2|^N and |s|^N stay bounded (PD_EINVAL).
 // Numerically checked against pivoted banded LU on every frequency of configs 0-2.
 // First-order recurrences with a *uniform* multiplier parallelise as chunked affine scans: a CTA owns one
@@ -79,7 +79,7 @@ PD_D void tri_tables(const pd_tri_coef& cf, double2* R2POW, double2* SPOW) {
 // Solve the Toeplitz system for the rows this thread holds in registers (d: right-hand side in, x out).
 // Thread k owns rows [k*L, k*L + Lk).  All NT threads must call (block scans, barriers).
 template <int NT>
-PD_D void tri_solve_regs(double2 (&d)[kL], const pd_tri_coef& cf, int Lk, int i0, const double2* R2POW,
+PD_D void tri_solve_regs(double2 (&d)[kL], const pd_tri_coef& cf, int Lk, int i0, int N, const double2* R2POW,
                          const double2* SPOW, double2* tot, double2* bc) {
   constexpr int L = kL;
   const int k = threadIdx.x;
@@ -107,32 +107,21 @@ PD_D void tri_solve_regs(double2 (&d)[kL], const pd_tri_coef& cf, int Lk, int i0
       d[j] = p;
     }
   }
-  // homogeneous response q (input w_i = r2^{i+1}): chunk-start value with zero carry-in
-  const double2 B = cmul(mtau, cpow_int(cf.r2, i0));  // -tau r2^{i0}
-  double2 pq = czero();
-  for (int j = Lk - 1; j >= 0; --j) pq = cfma(cf.s, pq, cmul(R2POW[j], B));
   const double2 Xin = block_affine_scan_excl<NT, true>(p, cf.sL, tot);
-  const double2 Qin = block_affine_scan_excl<NT, true>(pq, cf.sL, tot);
+  if (k == 0) bc[0] = cfma(SPOW[Lk], Xin, d[0]);  // x^(d)_0 (thread 0 holds row 0)
+  __syncthreads();
+  const double2 X0 = bc[0];
+  // rank-1 boundary correction in closed form (r02ac): the response of the backward recurrence to w_i = r2^{i+1} is
+  //   q_i = -tau sum_{k >= i} s^{k-i} r2^{k+1} = kappa (r2^{i+1} - r2^{N+1} s^{N-i}),  kappa = -tau / (1 - s r2),
+  // so x_i = x^(d)_i + c x_0 q_i = x^(d)_i + X0 (k1 r2^{i+1} + k2 s^{N-i}), k1 = c kappa / (1 - c q_0), k2 = -k1 r2^{N+1}
+  // (host, long double).  The s-term rides on the carry from above (s^{N-i} = s^{N-top} s^{top-i}), the r2-term on the
+  // chunk table: no second recurrence and no third block scan.
+  const int etop = N - i0 - Lk;
+  const double2 Xin2 = cfma(cmul(cf.k2, X0), cpow_int(cf.s, etop > 0 ? etop : 0), Xin);
+  const double2 Bg = cmul(cmul(cf.k1, X0), cpow_int(cf.r2, i0));
 #pragma unroll
   for (int j = 0; j < L; ++j)
-    if (j < Lk) d[j] = cfma(SPOW[Lk - j], Xin, d[j]);
-  if (k == 0) {
-    const double2 q0 = cfma(SPOW[Lk], Qin, pq);
-    const double2 x0 = cdiv(d[0], csub(make_double2(1.0, 0.0), cmul(cf.c, q0)));  // x^(d)_0 / (1 - c q_0)
-    bc[0] = cmul(cf.c, x0);
-  }
-  __syncthreads();
-  const double2 x0 = bc[0];  // c x_0
-  // x_i += (c x_0) q_i, q_i = q^loc_i + s^{Lk-j} Q_in, q^loc recomputed backward
-  pq = czero();
-#pragma unroll
-  for (int j = L - 1; j >= 0; --j) {
-    if (j < Lk) {
-      pq = cfma(cf.s, pq, cmul(R2POW[j], B));
-      const double2 q = cfma(SPOW[Lk - j], Qin, pq);
-      d[j] = cfma(x0, q, d[j]);
-    }
-  }
+    if (j < Lk) d[j] = cfma(R2POW[j], Bg, cfma(SPOW[Lk - j], Xin2, d[j]));
 }
 
 template <int NT>
@@ -166,7 +155,7 @@ __global__ void __launch_bounds__(NT) tridiag_kernel(double2* __restrict__ Sh, i
   double2 d[L];
 #pragma unroll
   for (int j = 0; j < L; ++j) d[j] = (j < Lk) ? sbuf[i0 + j + k] : czero();
-  tri_solve_regs<NT>(d, cf, Lk, i0, R2POW, SPOW, tot, bc);
+  tri_solve_regs<NT>(d, cf, Lk, i0, N, R2POW, SPOW, tot, bc);
   __syncthreads();  // staging buffer reuse
 #pragma unroll
   for (int j = 0; j < L; ++j)
@@ -211,7 +200,7 @@ __global__ void __launch_bounds__(NT) tail1d_kernel(const double* __restrict__ g
 #pragma unroll
       for (int t = 1; t < H; ++t) d[j] = cfma(hcn[t], make_double2(j < Lk ? __ldg(g + (long long)t * N + i0 + j) : 0.0, 0.0), d[j]);
     }
-    tri_solve_regs<NT>(d, cf, Lk, i0, R2POW, SPOW, tot, bc);
+    tri_solve_regs<NT>(d, cf, Lk, i0, N, R2POW, SPOW, tot, bc);
 #pragma unroll
     for (int a = 0; a < H; ++a)
 #pragma unroll
