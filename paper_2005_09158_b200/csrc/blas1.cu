@@ -53,11 +53,14 @@ PD_D void block_reduce_store(double (&acc)[K], double* partial) {
 // MODE 1: y <- a y + sum c_i X_i, then h_i = <X_i, y_new>     (y updated)
 // MODE 2: y <- a y + sum c_i X_i, then h_0 = <y_new, y_new>   (y updated; K vectors in, 1 output value)
 // MODE 3: y <- sum c_i X_i                                     (y written only, no reduction)
+// MODE 4: MODE 3 plus h_i = <X_i, y_new> and h_K = <y_new, y_new>
+// MODE 5: K = 1: h_0 = <y, y>, y <- y - X_0, h_1 = <y_new, y_new>   (the GMRES head fix with its two head norms)
 template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, double* __restrict__ y, long long n2,
                                                           double* __restrict__ partial, const double* tail_y,
                                                           long long n) {
-  constexpr int NACC = (MODE == 2 || MODE == 3) ? 1 : MODE == 4 ? K + 1 : K;  // mode 4: dots + ||y_new||^2
+  constexpr int NACC = (MODE == 2 || MODE == 3) ? 1 : MODE == 4 ? K + 1 : MODE == 5 ? 2 : K;  // mode 4: dots + ||y_new||^2
+  constexpr bool YIN = MODE <= 2 || MODE == 5;  // y is read
   // per-block contiguous range of double2 elements
   const long long per = (n2 + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * per, hi = min(n2, lo + per);
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
     for (int u = 0; u < U; ++u) {
       const long long t = t0 + (long long)u * kThreads;
       if (t < hi) {
-        yv[u] = MODE >= 3 ? czero() : reinterpret_cast<const double2*>(y)[t];
+        yv[u] = YIN ? reinterpret_cast<const double2*>(y)[t] : czero();
 #pragma unroll
         for (int i = 0; i < K; ++i) xv[u][i] = ld2_keep(X.p[i], t);
       }
@@ -84,7 +87,12 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
       const long long t = t0 + (long long)u * kThreads;
       if (t >= hi) break;
       double2 v = yv[u];
-      if constexpr (MODE >= 1) {
+      if constexpr (MODE == 5) {
+        acc[0] = fma(v.x, v.x, fma(v.y, v.y, acc[0]));
+        v = make_double2(v.x - xv[u][0].x, v.y - xv[u][0].y);
+        __stcs(reinterpret_cast<double2*>(y) + t, v);
+        acc[1] = fma(v.x, v.x, fma(v.y, v.y, acc[1]));
+      } else if constexpr (MODE >= 1) {
         double2 nv = MODE >= 3 ? czero() : make_double2(a * v.x, a * v.y);
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -96,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
       }
       if constexpr (MODE == 2) {
         acc[0] = fma(v.x, v.x, fma(v.y, v.y, acc[0]));
-      } else if constexpr (MODE != 3) {
+      } else if constexpr (MODE != 3 && MODE != 5) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = fma(xv[u][i].x, v.x, fma(xv[u][i].y, v.y, acc[i]));
         if constexpr (MODE == 4) acc[NACC - 1] = fma(v.x, v.x, fma(v.y, v.y, acc[NACC - 1]));
@@ -107,8 +115,13 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
   if (n & 1) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const long long t = n - 1;
-      double yv = MODE >= 3 ? 0.0 : y[t];
-      if constexpr (MODE >= 1) {
+      double yv = YIN ? y[t] : 0.0;
+      if constexpr (MODE == 5) {
+        acc[0] = fma(yv, yv, acc[0]);
+        yv -= X.p[0][t];
+        y[t] = yv;
+        acc[1] = fma(yv, yv, acc[1]);
+      } else if constexpr (MODE >= 1) {
         double nv = MODE >= 3 ? 0.0 : a * yv;
 #pragma unroll
         for (int i = 0; i < K; ++i) nv = fma(X.c[i], X.p[i][t], nv);
@@ -117,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
       }
       if constexpr (MODE == 2) {
         acc[0] = fma(yv, yv, acc[0]);
-      } else if constexpr (MODE != 3) {
+      } else if constexpr (MODE != 3 && MODE != 5) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = fma(X.p[i][t], yv, acc[i]);
         if constexpr (MODE == 4) acc[NACC - 1] = fma(yv, yv, acc[NACC - 1]);
@@ -189,6 +202,11 @@ cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coe
   if (mode == 1) return krylov_launch<1>(pk, k, a, y, n, partial, st);
   if (mode == 2) return krylov_launch<2>(pk, k, a, y, n, partial, st);
   if (mode == 4) return krylov_launch<4>(pk, k, a, y, n, partial, st);
+  if (mode == 5) {
+    if (k != 1) return cudaErrorInvalidValue;
+    krylov_kernel<1, 5><<<kBlocks, kThreads, 0, st>>>(pk, a, y, n / 2, partial, nullptr, n);
+    return cudaGetLastError();
+  }
   return krylov_launch<3>(pk, k, a, y, n, partial, st);
 }
 

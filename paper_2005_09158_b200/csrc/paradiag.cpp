@@ -943,7 +943,7 @@ pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double*
   phase_begin(c, 6);
   PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st));
   if (mode != 3) {
-    const int kk = mode == 2 ? 1 : mode == 4 ? k + 1 : k;
+    const int kk = mode == 2 ? 1 : mode == 4 ? k + 1 : mode == 5 ? 2 : k;
     PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), kk, c->dred, c->st));
     phase_end(c, 6);
     if (global_sum && c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
@@ -1174,7 +1174,9 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
   const bool corner = c->sten.g3 == 0.0 && c->sten.g1 == 0.0 && gcorner.H >= 1 && c->nt >= 2 * gcorner.H &&
                       getenv("PD_GMRES_MATVEC") == nullptr;
   const long long hn_len = (long long)gcorner.H * c->S;
-  std::vector<double> eh(m + 1);
+  std::vector<double> eh(m + 2);
+  std::vector<const double*> Xh(m + 2);
+  const bool lazy_last = getenv("PD_GMRES_NO_LAZY") == nullptr;
   double ww_known = -1.0;                 // ||w||^2 when the second CGS pass is skipped
   const double kReorthSkip = getenv("PD_GMRES_ALWAYS_CGS2") ? -1.0 : 1e-12;
   double* dhead = nullptr;
@@ -1211,6 +1213,7 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
       }
       ++its;
       double* w = c->V[j + 1];
+      bool skip_vector = false;  // corner path: the cycle ends at this column, V_{j+1} is not assembled
       if (corner) {
         // A P^{-1} X_j = X_j - E_H G tail(P^{-1} X_j)  ((P - A) touches only head rows x tail columns, the identity
         // behind the tail form): the matvec sweep disappears and, the basis being orthonormal, the first CGS pass is
@@ -1218,26 +1221,52 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
         // projections of the assembled w as before, so orthogonality is enforced to working precision.
         s = pd_corner_head(c, gcorner, zj + (long long)(c->nt - gcorner.H) * c->S, dhead);
         if (s != PD_OK) return s;
-        s = pd_krylov_n(c, 0, Xp, nullptr, j + 1, 0.0, dhead, hn_len, eh.data());  // <X_i[head], G tail>
+        // <X_i[head], G tail>, and ||G tail||^2 as one more dot of the same launch
+        for (int i = 0; i <= j; ++i) Xh[i] = Xp[i];
+        Xh[j + 1] = dhead;
+        s = pd_krylov_n(c, 0, Xh.data(), nullptr, j + 2, 0.0, dhead, hn_len, eh.data());
         if (s != PD_OK) return s;
         for (int i = 0; i <= j; ++i) {
           h[i] = (i == j ? 1.0 : 0.0) - sc[i] * sc[j] * eh[i];
           coef[i] = -h[i] * sc[i] / sc[j];
         }
+        // The new basis vector is only needed by a further iteration of this cycle.  Its norm follows from head-sized
+        // numbers: w - sum h_i V_i = -(I - V V^T) E_H c, c = sc_j G tail, so ||.||^2 = sc_j^2 (||G tail||^2 -
+        // sum_i sc_i^2 <X_i[head], G tail>^2) for an orthonormal basis.  When that estimate (trusted only while the
+        // subtraction keeps 8 digits) says the cycle ends here - converged by the Arnoldi estimate, clear of the
+        // threshold, or j = m - 1 - the sweep that would assemble the vector (j + 2 vector moves) is skipped; the true
+        // residual at the cycle end still decides (reading c6).  PD_GMRES_NO_LAZY=1 always assembles it.
+        if (lazy_last) {
+          double pe = 0.0;
+          for (int i = 0; i <= j; ++i) pe += sc[i] * sc[i] * eh[i] * eh[i];
+          const double dd = eh[j + 1], wwe = dd - pe;
+          if (dd > 0.0 && wwe > 1e-8 * dd) {
+            const double hne = sc[j] * std::sqrt(wwe);
+            std::vector<double> col(h.begin(), h.begin() + j + 1);
+            for (int i = 0; i < j; ++i) {
+              const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+              col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+              col[i] = t;
+            }
+            const double gn = std::fabs(hne / std::hypot(col[j], hne) * gv[j]);  // |gv[j+1]| after the j-th rotation
+            const double thr = tol * bnorm;
+            const bool done = gn <= 0.5 * thr, undecided = gn > 0.5 * thr && gn <= 2.0 * thr;
+            if (done || (j == m - 1 && !undecided)) {
+              ww_known = wwe;
+              skip_vector = true;
+            }
+          }
+        }
+        if (!skip_vector) {
         coef[j] = sc[j] * sc[j] * eh[j];  // 1 - h_jj without cancellation: w_raw = X_j + E_H delta - sum h_i sc_i/sc_j X_i
         s = pd_krylov_n(c, 4, Xp, coef.data(), j + 1, 0.0, w, n, h2.data());  // written fresh: dots + ||.||^2
         if (s != PD_OK) return s;
         // + E_H delta (delta = -G tail); ||w||^2 updated from the head before/after (head-sized dots)
-        double hb = 0, ha = 0;
-        const double* wv[1] = {w};
-        s = pd_krylov_n(c, 0, wv, nullptr, 1, 0.0, w, hn_len, &hb);
+        double hba[2] = {0, 0};  // head norms before / after w[head] -= G tail, one launch (krylov mode 5)
+        const double* hx[1] = {dhead};
+        s = pd_krylov_n(c, 5, hx, nullptr, 1, 0.0, w, hn_len, hba);
         if (s != PD_OK) return s;
-        const double* hx[2] = {w, dhead};
-        const double hc[2] = {1.0, -1.0};
-        s = pd_krylov_n(c, 3, hx, hc, 2, 0.0, w, hn_len, nullptr);
-        if (s != PD_OK) return s;
-        s = pd_krylov_n(c, 0, wv, nullptr, 1, 0.0, w, hn_len, &ha);
-        if (s != PD_OK) return s;
+        const double hb = hba[0], ha = hba[1];
         const double ww1 = std::max(0.0, h2[j + 1] - hb + ha);
         double pmax = 0.0;
         for (int i = 0; i <= j; ++i) {
@@ -1253,6 +1282,7 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
             h[i] += h2[i];
           }
         }
+        }  // !skip_vector
       } else {
         s = pd_stencil_impl(c, nullptr, zj, w, nullptr);
         if (s != PD_OK) return s;
@@ -1296,7 +1326,7 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
       gv[j] = cs[j] * gv[j];
       kk = j + 1;
       pd_report_push(rep, std::fabs(gv[j + 1]) / bnorm);
-      if (std::fabs(gv[j + 1]) <= tol * bnorm || its >= maxit) break;
+      if (std::fabs(gv[j + 1]) <= tol * bnorm || its >= maxit || skip_vector) break;
       if (hn == 0.0) {
         breakdown = true;
         break;

@@ -335,6 +335,35 @@ def test_gmres_final_assembly_variants_agree(monkeypatch, name):
         assert r1.iterations == rep_ref.iterations and rel(u1, u_ref) < SOLVE_TOL
 
 
+@pytest.mark.parametrize("name", ["cfg4s", "cfg1", "cfg3s"])
+def test_gmres_lazy_last_vector_matches_assembled(monkeypatch, name):
+    """The corner-identity GMRES does not assemble the basis vector of a column that ends its cycle (converged by the
+    Arnoldi estimate, or j = m - 1): its norm comes from head-sized dots.  PD_GMRES_NO_LAZY=1 always assembles it.
+    Same iterations and residual histories (the estimate and the measured norm agree to ~1e-8), same solution, for
+    the configured m and for restarted runs (m = 2, 3: every cycle ends at j = m - 1)."""
+    cfg = {"cfg4s": W.BY_NAME["cfg4"].scaled(nx=64, ny=64, nt=1024), "cfg1": W.BY_NAME["cfg1"],
+           "cfg3s": W.BY_NAME["cfg3"].scaled(nx=64, ny=64, nt=256)}[name]
+    for m in (cfg.m, 2, 3):
+        outs = []
+        for env in (None, "1"):
+            monkeypatch.delenv("PD_GMRES_NO_LAZY", raising=False)
+            if env:
+                monkeypatch.setenv("PD_GMRES_NO_LAZY", env)
+            ctx = make_ctx(cfg)
+            b = ctx.build_rhs(to_dev(W.initial_u0(cfg)), None,
+                              None if W.source_samples(cfg) is None else to_dev(W.source_samples(cfg)))
+            u, rep = ctx.solve_gmres(b, tol=cfg.tol, m=m, maxit=cfg.maxit)
+            outs.append((to_host(u), rep))
+            bh = to_host(b)
+        (u1, r1), (u2, r2) = outs
+        assert r1.converged and r2.converged and r1.iterations == r2.iterations, (m, r1.history, r2.history)
+        for a, c in zip(r1.history, r2.history):
+            assert abs(a - c) <= 1e-6 * max(a, c) + 1e-16, (m, r1.history, r2.history)
+        assert rel(u1, u2) < 1e-10
+        u_ref, rep_ref = solvers.solve_gmres(cfg, bh, m=m)
+        assert r1.iterations == rep_ref.iterations and rel(u1, u_ref) < SOLVE_TOL
+
+
 def test_gmres_fused_bnorm_matches_separate_dot(monkeypatch):
     """Zero initial guess on the 2D four-step path: ||b|| taken by the first apply's Step (a) read of b (default) vs
     a separate dot sweep (PD_GMRES_NO_FUSED_NORM=1): same iterations, solutions and residual within rounding (the
