@@ -54,13 +54,14 @@ PD_D void block_reduce_store(double (&acc)[K], double* partial) {
 // MODE 2: y <- a y + sum c_i X_i, then h_0 = <y_new, y_new>   (y updated; K vectors in, 1 output value)
 // MODE 3: y <- sum c_i X_i                                     (y written only, no reduction)
 // MODE 4: MODE 3 plus h_i = <X_i, y_new> and h_K = <y_new, y_new>
-// MODE 5: K = 1: h_0 = <y, y>, y <- y - X_0, h_1 = <y_new, y_new>   (the GMRES head fix with its two head norms)
 template <int K, int MODE>
+// hsub / hlen (MODE 4): y_new[t] -= hsub[t] for t < hlen before the dots (the GMRES head fix w[head] -= G tail fused
+// into the sweep that writes w)
 __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, double* __restrict__ y, long long n2,
-                                                          double* __restrict__ partial, const double* tail_y,
-                                                          long long n) {
-  constexpr int NACC = (MODE == 2 || MODE == 3) ? 1 : MODE == 4 ? K + 1 : MODE == 5 ? 2 : K;  // mode 4: dots + ||y_new||^2
-  constexpr bool YIN = MODE <= 2 || MODE == 5;  // y is read
+                                                          double* __restrict__ partial, const double* __restrict__ hsub,
+                                                          long long hlen, long long n) {
+  constexpr int NACC = (MODE == 2 || MODE == 3) ? 1 : MODE == 4 ? K + 1 : K;  // mode 4: dots + ||y_new||^2
+  constexpr bool YIN = MODE <= 2;  // y is read
   // per-block contiguous range of double2 elements
   const long long per = (n2 + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * per, hi = min(n2, lo + per);
@@ -87,24 +88,23 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
       const long long t = t0 + (long long)u * kThreads;
       if (t >= hi) break;
       double2 v = yv[u];
-      if constexpr (MODE == 5) {
-        acc[0] = fma(v.x, v.x, fma(v.y, v.y, acc[0]));
-        v = make_double2(v.x - xv[u][0].x, v.y - xv[u][0].y);
-        __stcs(reinterpret_cast<double2*>(y) + t, v);
-        acc[1] = fma(v.x, v.x, fma(v.y, v.y, acc[1]));
-      } else if constexpr (MODE >= 1) {
+      if constexpr (MODE >= 1) {
         double2 nv = MODE >= 3 ? czero() : make_double2(a * v.x, a * v.y);
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           nv.x = fma(X.c[i], xv[u][i].x, nv.x);
           nv.y = fma(X.c[i], xv[u][i].y, nv.y);
         }
+        if constexpr (MODE == 4) {
+          if (2 * t < hlen) nv.x -= hsub[2 * t];
+          if (2 * t + 1 < hlen) nv.y -= hsub[2 * t + 1];
+        }
         v = nv;
         __stcs(reinterpret_cast<double2*>(y) + t, v);
       }
       if constexpr (MODE == 2) {
         acc[0] = fma(v.x, v.x, fma(v.y, v.y, acc[0]));
-      } else if constexpr (MODE != 3 && MODE != 5) {
+      } else if constexpr (MODE != 3) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = fma(xv[u][i].x, v.x, fma(xv[u][i].y, v.y, acc[i]));
         if constexpr (MODE == 4) acc[NACC - 1] = fma(v.x, v.x, fma(v.y, v.y, acc[NACC - 1]));
@@ -116,28 +116,25 @@ __global__ void __launch_bounds__(kThreads) krylov_kernel(PtrPack X, double a, d
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const long long t = n - 1;
       double yv = YIN ? y[t] : 0.0;
-      if constexpr (MODE == 5) {
-        acc[0] = fma(yv, yv, acc[0]);
-        yv -= X.p[0][t];
-        y[t] = yv;
-        acc[1] = fma(yv, yv, acc[1]);
-      } else if constexpr (MODE >= 1) {
+      if constexpr (MODE >= 1) {
         double nv = MODE >= 3 ? 0.0 : a * yv;
 #pragma unroll
         for (int i = 0; i < K; ++i) nv = fma(X.c[i], X.p[i][t], nv);
+        if constexpr (MODE == 4) {
+          if (t < hlen) nv -= hsub[t];
+        }
         yv = nv;
         y[t] = yv;
       }
       if constexpr (MODE == 2) {
         acc[0] = fma(yv, yv, acc[0]);
-      } else if constexpr (MODE != 3 && MODE != 5) {
+      } else if constexpr (MODE != 3) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = fma(X.p[i][t], yv, acc[i]);
         if constexpr (MODE == 4) acc[NACC - 1] = fma(yv, yv, acc[NACC - 1]);
       }
     }
   }
-  (void)tail_y;
   if constexpr (MODE != 3) block_reduce_store<NACC>(acc, partial);
 }
 
@@ -165,12 +162,13 @@ __global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const double*
 }
 
 template <int MODE>
-cudaError_t krylov_launch(const PtrPack& pk, int k, double a, double* y, long long n, double* partial, cudaStream_t st) {
+cudaError_t krylov_launch(const PtrPack& pk, int k, double a, double* y, long long n, double* partial, cudaStream_t st,
+                          const double* hsub = nullptr, long long hlen = 0) {
   const long long n2 = n / 2;
   switch (k) {
 #define PD_K(K)                                                                              \
   case K:                                                                                    \
-    krylov_kernel<K, MODE><<<kBlocks, kThreads, 0, st>>>(pk, a, y, n2, partial, nullptr, n); \
+    krylov_kernel<K, MODE><<<kBlocks, kThreads, 0, st>>>(pk, a, y, n2, partial, hsub, hlen, n); \
     break;
     PD_K(1) PD_K(2) PD_K(3) PD_K(4) PD_K(5) PD_K(6) PD_K(7) PD_K(8) PD_K(9) PD_K(10) PD_K(11) PD_K(12) PD_K(13)
     PD_K(14) PD_K(15) PD_K(16) PD_K(17) PD_K(18) PD_K(19) PD_K(20) PD_K(21) PD_K(22) PD_K(23) PD_K(24) PD_K(25)
@@ -189,7 +187,7 @@ int pd_blas_blocks() { return kBlocks; }
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coef, int k, double a, double* y,
-                             long long n, double* partial, cudaStream_t st) {
+                             long long n, double* partial, cudaStream_t st, const double* hsub, long long hlen) {
   if (k < 1 || k > kMaxK) return cudaErrorInvalidValue;
   PtrPack pk = {};
   for (int i = 0; i < k; ++i) {
@@ -201,12 +199,7 @@ cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coe
   if (mode == 0) return krylov_launch<0>(pk, k, a, y, n, partial, st);
   if (mode == 1) return krylov_launch<1>(pk, k, a, y, n, partial, st);
   if (mode == 2) return krylov_launch<2>(pk, k, a, y, n, partial, st);
-  if (mode == 4) return krylov_launch<4>(pk, k, a, y, n, partial, st);
-  if (mode == 5) {
-    if (k != 1) return cudaErrorInvalidValue;
-    krylov_kernel<1, 5><<<kBlocks, kThreads, 0, st>>>(pk, a, y, n / 2, partial, nullptr, n);
-    return cudaGetLastError();
-  }
+  if (mode == 4) return krylov_launch<4>(pk, k, a, y, n, partial, st, hsub, hsub ? hlen : 0);
   return krylov_launch<3>(pk, k, a, y, n, partial, st);
 }
 

@@ -192,7 +192,8 @@ pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate);
 pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* out, double* norm2);
 // reduced values are all-reduced across NCCL ranks unless global_sum is false (vectors replicated on every rank)
 pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a, double* y,
-                      long long n, double* host_out, bool global_sum = true);
+                      long long n, double* host_out, bool global_sum = true, const double* hsub = nullptr,
+                      long long hlen = 0);
 extern "C" void pd_report_push(pd_report* rep, double v);
 void pd_tail_free(pd_ctx* c);
 void pd_corner_coefs(const pd_ctx* c, pd_tail_g* gc);

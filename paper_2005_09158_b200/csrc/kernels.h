@@ -215,10 +215,13 @@ cudaError_t pd_launch_rhs(const pd_stencil& p, const double* u0, const double* v
 int pd_blas_blocks();
 // mode 0: partial <- <X_i, y>;  1: y <- a y + sum c_i X_i, partial <- <X_i, y_new>;
 // mode 2: y <- a y + sum c_i X_i, partial <- <y_new, y_new>;  3: y <- sum c_i X_i;
-// mode 4: y <- sum c_i X_i (y not read), partial <- (<X_i, y_new>, <y_new, y_new>)  (K' = k + 1).
-// partial[blk * K' + i], K' = k (modes 0, 1) or 1 (mode 2); coef on the host.  All vectors 16-byte aligned.
+// mode 4: y <- sum c_i X_i (y not read) [- hsub on the first hlen elements], partial <- (<X_i, y_new>, <y_new, y_new>)
+// (K' = k + 1).
+// partial[blk * K' + i], K' = k (modes 0, 1) or 1 (mode 2); coef on the host.  All vectors 16-byte aligned
+// (hsub: any alignment).
 cudaError_t pd_launch_krylov(int mode, const double* const* X, const double* coef, int k, double a, double* y,
-                             long long n, double* partial, cudaStream_t st);
+                             long long n, double* partial, cudaStream_t st, const double* hsub = nullptr,
+                             long long hlen = 0);
 // sum partials in fixed order: out[i] = sum_blk partial[blk*k + i]  (device out)
 cudaError_t pd_launch_reduce_partials(const double* partial, int nblk, int k, double* out, cudaStream_t st);
 // y = a x + b y

@@ -939,11 +939,11 @@ pd_status pd_stencil_impl(pd_ctx* c, const double* b, const double* u, double* o
 // Krylov sweep (blas1.cu) over the local vector; the k (or 1) reduced values all-reduced across ranks and
 // copied to host_out (syncs) unless host_out == NULL (mode 3)
 pd_status pd_krylov_n(pd_ctx* c, int mode, const double* const* X, const double* coef, int k, double a, double* y,
-                      long long n, double* host_out, bool global_sum) {
+                      long long n, double* host_out, bool global_sum, const double* hsub, long long hlen) {
   phase_begin(c, 6);
-  PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st));
+  PD_LAUNCH(c, pd_launch_krylov(mode, X, coef, k, a, y, n, c->partial, c->st, hsub, hlen));
   if (mode != 3) {
-    const int kk = mode == 2 ? 1 : mode == 4 ? k + 1 : mode == 5 ? 2 : k;
+    const int kk = mode == 2 ? 1 : mode == 4 ? k + 1 : k;
     PD_LAUNCH(c, pd_launch_reduce_partials(c->partial, pd_blas_blocks(), kk, c->dred, c->st));
     phase_end(c, 6);
     if (global_sum && c->dist_mode == 1 && pd_comm_allreduce_sum(c->comm, c->dred, kk) != 0)
@@ -1259,18 +1259,14 @@ static pd_status gmres_impl(pd_ctx* c, const double* b, double* u, double tol, i
         }
         if (!skip_vector) {
         coef[j] = sc[j] * sc[j] * eh[j];  // 1 - h_jj without cancellation: w_raw = X_j + E_H delta - sum h_i sc_i/sc_j X_i
-        s = pd_krylov_n(c, 4, Xp, coef.data(), j + 1, 0.0, w, n, h2.data());  // written fresh: dots + ||.||^2
+        // written fresh, + E_H delta (delta = -G tail) on the head rows inside the same sweep: the dots and ||w||^2
+        // are those of the final vector
+        s = pd_krylov_n(c, 4, Xp, coef.data(), j + 1, 0.0, w, n, h2.data(), true, dhead, hn_len);
         if (s != PD_OK) return s;
-        // + E_H delta (delta = -G tail); ||w||^2 updated from the head before/after (head-sized dots)
-        double hba[2] = {0, 0};  // head norms before / after w[head] -= G tail, one launch (krylov mode 5)
-        const double* hx[1] = {dhead};
-        s = pd_krylov_n(c, 5, hx, nullptr, 1, 0.0, w, hn_len, hba);
-        if (s != PD_OK) return s;
-        const double hb = hba[0], ha = hba[1];
-        const double ww1 = std::max(0.0, h2[j + 1] - hb + ha);
+        const double ww1 = h2[j + 1];
         double pmax = 0.0;
         for (int i = 0; i <= j; ++i) {
-          h2[i] = sc[i] * sc[j] * (h2[i] - eh[i]);
+          h2[i] = sc[i] * sc[j] * h2[i];
           pmax = std::max(pmax, std::fabs(h2[i]));
         }
         if (pmax <= kReorthSkip * sc[j] * std::sqrt(ww1)) {

@@ -1,4 +1,4 @@
-# r02ae: GMRES head fix as one launch (krylov mode 5): GMRES parity subset, bench lines cfg1 / cfg3 / cfg4
+# r02ae: GMRES head fix fused into the mode-4 sweep: GMRES parity subset, bench lines cfg1 / cfg3 / cfg4
 source tools/gpu_preflight.sh
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dist.py -m gpu -x -q -k "gmres or solve_full or dist" > gpurun_out/r02ae_tests.log 2>&1; tail -3 gpurun_out/r02ae_tests.log
