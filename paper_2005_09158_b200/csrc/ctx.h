@@ -122,7 +122,9 @@ struct pd_ctx {
   // host-buffer staging
   double* stage_a = nullptr;
   double* stage_b = nullptr;
-  // CUDA graphs of the apply, keyed by (r, z, accumulate) (PD_GRAPH=1)
+  // CUDA graphs of the apply, keyed by (r, z, accumulate).  PD_GRAPH=1: captured at the first use of a triple;
+  // default for launch-bound sizes (Nt S <= 2^21: configs 0 and 1): captured at its SECOND use (exec == nullptr marks a
+  // triple seen once), so a one-off solve never pays for an instantiation; PD_GRAPH=0: never
   struct GraphEntry {
     const double* r;
     double* z;
@@ -132,6 +134,7 @@ struct pd_ctx {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = false;
+  bool graphs_on_reuse = false;
   cudaStream_t cap_stream = nullptr;  // private stream for capture (the legacy stream cannot capture)
   // WR tail form (tailform.cpp), built on first use
   struct TailState {

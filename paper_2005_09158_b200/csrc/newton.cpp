@@ -18,7 +18,8 @@ pd_status pd_set_reaction(pd_ctx* c, double g3, double g1) {
     return fail(c, PD_EINVAL, "reaction terms: 1D operators with the theta-method only");
   c->sten.g3 = g3;
   c->sten.g1 = g1;
-  for (auto& gr : c->graphs) cudaGraphExecDestroy(gr.exec);  // captured applies baked in the old operator
+  for (auto& gr : c->graphs)
+    if (gr.exec) cudaGraphExecDestroy(gr.exec);  // captured applies baked in the old operator
   c->graphs.clear();
   return PD_OK;
 }

@@ -248,7 +248,8 @@ static void free_ctx(pd_ctx* c) {
     if (p) cudaFree(p);
   for (double* p : c->V) cudaFree(p);
   if (c->hred) cudaFreeHost(c->hred);
-  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto& g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (int k = 1; k < kPdMaxOverlap; ++k) {
     if (c->ov.scratch[k]) cudaFree(c->ov.scratch[k]);
@@ -568,7 +569,14 @@ pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme 
   // ---- four-step time FFT for long time axes (1D), or with the x-FFT folded in (2D, tfx.cu) ----
   c->use_tfx = g->op == PD_ADE2D_PERIODIC && pd_tfx_supported(nt, g->nx) && getenv("PD_NO_TFX") == nullptr;
   c->use_tf4 = !c->use_tfx && pd_tf4_supported(nt) && getenv("PD_NO_TF4") == nullptr;
-  c->use_graphs = getenv("PD_GRAPH") != nullptr && atoi(getenv("PD_GRAPH")) != 0;
+  if (const char* ge = getenv("PD_GRAPH")) {
+    c->use_graphs = atoi(ge) != 0;
+  } else {
+    // launch-bound sizes (configs 0 and 1): replay a triple's launch sequence from its second use on (apply -22 %,
+    // r02ah).  Not beyond ~2M dofs: at the config-2/3 size the replay gains 2 % per apply and instantiating the ~50-node
+    // multi-stream graph costs ~1 ms per triple (r02ai: cfg3 e2e 3.9 -> 5.0 ms over the bench's repetitions)
+    c->use_graphs = c->graphs_on_reuse = (long long)nt * c->S <= (1LL << 21);
+  }
   if (c->use_tf4 || c->use_tfx) {
     const int n2 = c->use_tfx ? pd_tfx_n2(nt) : pd_tf4_n2(), n1 = nt / n2;
     const long long align = c->use_tfx ? pd_tfx_chunk_align(nt, g->nx) : pd_tf4_pairs_per_tile();
@@ -882,15 +890,25 @@ static pd_status apply_with_norm(pd_ctx* c, const double* r, double* z, double* 
 // launch sequence of each (r, z, accumulate) triple is captured once and replayed as one CUDA graph.
 pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
   if (!c->use_graphs || c->dist_mode != 0 || c->timing) return apply_direct(c, r, z, accumulate);
+  pd_ctx::GraphEntry* seen = nullptr;
   for (auto& g : c->graphs)
     if (g.r == r && g.z == z && g.acc == accumulate) {
+      if (!g.exec) {
+        seen = &g;  // second use of the triple: capture now
+        break;
+      }
       PD_CUDA(c, cudaGraphLaunch(g.exec, c->st));
       c->launches += g.launches;
       return PD_OK;
     }
-  if (c->graphs.size() >= 64) {
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (!seen && c->graphs.size() >= 64) {
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+  }
+  if (!seen && c->graphs_on_reuse) {  // first use: run directly, remember the triple
+    c->graphs.push_back({r, z, accumulate, nullptr, 0});
+    return apply_direct(c, r, z, accumulate);
   }
   const long long l0 = c->launches;
   if (!c->cap_stream) PD_CUDA(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
@@ -907,7 +925,12 @@ pd_status pd_apply_impl(pd_ctx* c, const double* r, double* z, int accumulate) {
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return fail(c, PD_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
-  c->graphs.push_back({r, z, accumulate, exec, c->launches - l0});
+  if (seen) {
+    seen->exec = exec;
+    seen->launches = c->launches - l0;
+  } else {
+    c->graphs.push_back({r, z, accumulate, exec, c->launches - l0});
+  }
   PD_CUDA(c, cudaGraphLaunch(exec, c->st));
   return PD_OK;
 }

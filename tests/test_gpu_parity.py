@@ -113,12 +113,17 @@ def test_apply_time_fft_pipeline_variants(monkeypatch, op, scheme, nx, nt, kov, 
     check_apply(cfg, r, z)
 
 
+@pytest.mark.parametrize("mode", ["1", None])
 @pytest.mark.parametrize("op,scheme,nx,nt", [(W.ADE2D, W.CN, 64, 1024), (W.ADE1D, W.CN, 1023, 1024)])
-def test_apply_graph_replay(monkeypatch, op, scheme, nx, nt):
+def test_apply_graph_replay(monkeypatch, op, scheme, nx, nt, mode):
     """PD_GRAPH=1: the first apply of an (r, z) pair is captured (with the time-FFT stream pipeline's fork/join
-    as parallel branches) and every later one replays the graph; the replays see new contents of r."""
+    as parallel branches) and every later one replays the graph; the replays see new contents of r.  Default
+    (PD_GRAPH unset) at these launch-bound sizes: the first use of a pair runs directly, the second is captured,
+    later ones replay."""
     import torch
-    monkeypatch.setenv("PD_GRAPH", "1")
+    monkeypatch.delenv("PD_GRAPH", raising=False)
+    if mode:
+        monkeypatch.setenv("PD_GRAPH", mode)
     cfg = _cfg(op, scheme, nx, nt, alpha=0.02)
     ctx = make_ctx(cfg)
     r1, r2 = W.random_vector(cfg, seed=1), W.random_vector(cfg, seed=2)
@@ -130,6 +135,8 @@ def test_apply_graph_replay(monkeypatch, op, scheme, nx, nt):
     check_apply(cfg, r1, to_host(zd))
     rd.copy_(to_dev(r2))
     ctx.apply_precond(rd, zd)            # replay on new data
+    check_apply(cfg, r2, to_host(zd))
+    ctx.apply_precond(rd, zd)
     check_apply(cfg, r2, to_host(zd))
 
 

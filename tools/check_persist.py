@@ -2,6 +2,7 @@
 outputs agree to rounding; phase times per call (0 = forward, 1 = Step (b), 2 = inverse).  argv: config [reps]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["PD_GRAPH"] = "0"  # the same (r, z) pair runs both modes: no replay of the first one captured
 import torch
 import workloads as W
 from tests.helpers import make_ctx
