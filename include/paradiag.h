@@ -103,7 +103,12 @@ typedef struct {
  * For Nt >= 1024 the context also owns up to three internal non-blocking streams and their scratch chunks (the time-FFT
  * chunk pipeline); every call still behaves as if ordered on cuda_stream (event fork / join).
  * Tuning environment (read here, at setup): PD_TF4_OVERLAP / PD_TF4_OVERLAP_INV (streams of the forward /
- * inverse time FFT, default 3 / 4), PD_TF4_CHUNK_MB, PD_GRAPH.
+ * inverse time FFT, default 3 / 4), PD_TF4_CHUNK_MB, PD_GRAPH (CUDA-graph replay of the apply: unset = for Nt * S <= 2^21
+ * from the second use of an (r, z) pair, 1 = always, 0 = never; a replay bakes in the pointers and the launch path of
+ * the capture).  Read per call (A/B switches of measured alternatives; the defaults are the measured
+ * best): PD_GMRES_NO_LAZY, PD_GMRES_NO_Z, PD_GMRES_MATVEC (GMRES variants), PD_DST_FULL, PD_DST_CHUNK_MB (2D Dirichlet
+ * x-DST rows), PD_TFX_PERSIST, PD_TFX_LAG (persistent fused time FFT; experimental: its scratch ring is one per
+ * process and device, so run one context at a time with it).
  * Returns PD_EINVAL / PD_ESINGULAR / PD_ENOMEM / PD_ECUDA / PD_ENCCL on failure (*out = NULL). */
 PD_API pd_status pd_setup(const pd_grid* g, double dt, int nt, double alpha, pd_scheme s, const pd_dist* dist,
                    void* cuda_stream, pd_ctx** out);
