@@ -14,6 +14,26 @@
 #include "fft.cuh"
 #include "kernels.h"
 
+// L2 policy of the y-pass tile loads / stores (slab_ytri_kernel, dtri_kernel): 1 = ld.cg / st.cg, 0 = evict-first
+// (ld.cs / st.cs).  Measured (r02al/am, cfg4 y-pass): evict-first loads 2.01 ms, ld.cg loads 1.72 ms, the store policy
+// makes no difference; so the tiles are loaded with ld.cg and stored evict-first (the inverse time FFT that follows
+// wants its L2 for the four-step scratch)
+#ifndef PD_SPEC_KEEP_SLAB_LD
+#define PD_SPEC_KEEP_SLAB_LD 1
+#endif
+#ifndef PD_SPEC_KEEP_SLAB_ST
+#define PD_SPEC_KEEP_SLAB_ST 0
+#endif
+#if PD_SPEC_KEEP_SLAB_LD
+#define PD_SPEC_LD(p) __ldcg(p)
+#else
+#define PD_SPEC_LD(p) __ldcs(p)
+#endif
+#if PD_SPEC_KEEP_SLAB_ST
+#define PD_SPEC_ST(p, v) __stcg(p, v)
+#else
+#define PD_SPEC_ST(p, v) __stcs(p, v)
+#endif
 using namespace pdfft;
 
 namespace {
@@ -435,7 +455,7 @@ __global__ void __launch_bounds__(32 * kYC, PD_YTRI_MINB ? PD_YTRI_MINB : (N <= 
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
       const int i = threadIdx.x + k * 32 * kYC, r = i / kYC, c = i % kYC;
-      v[k] = __ldcs(slab + (long long)r * N + c);
+      v[k] = PD_SPEC_LD(slab + (long long)r * N + c);
     }
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(32 * kYC, PD_YTRI_MINB ? PD_YTRI_MINB : (N <= 
 #pragma unroll 8
   for (int i = threadIdx.x; i < N * kYC; i += 32 * kYC) {
     const int r = i / kYC, c = i % kYC;
-    __stcs(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
+    PD_SPEC_ST(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
   }
 }
 
@@ -551,7 +571,7 @@ dtri_kernel(double2* __restrict__ Sh, int slab0, int fglob0, const pd_dtri_coef*
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
       const int i = threadIdx.x + k * 32 * kYC, r = i / kYC, c = i % kYC;
-      v[k] = (r < N && c0 + c < N) ? __ldcs(slab + (long long)r * N + c) : czero();
+      v[k] = (r < N && c0 + c < N) ? PD_SPEC_LD(slab + (long long)r * N + c) : czero();
     }
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
@@ -623,7 +643,7 @@ dtri_kernel(double2* __restrict__ Sh, int slab0, int fglob0, const pd_dtri_coef*
 #pragma unroll 4
   for (int i = threadIdx.x; i < N * kYC; i += 32 * kYC) {
     const int r = i / kYC, c = i % kYC;
-    if (c0 + c < N) __stcs(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
+    if (c0 + c < N) PD_SPEC_ST(slab + (long long)r * N + c, sm[c * CS + r + r / L]);
   }
 }
 
