@@ -16,7 +16,7 @@
 
 // L2 policy of the y-pass tile loads / stores (slab_ytri_kernel, dtri_kernel): 1 = ld.cg / st.cg, 0 = evict-first
 // (ld.cs / st.cs).  Measured (r02al/am, cfg4 y-pass): evict-first loads 2.01 ms, ld.cg loads 1.72 ms, the store policy
-// makes no difference; so the tiles are loaded with ld.cg and stored evict-first (the inverse time FFT that follows
+// makes no difference, ld.lu loads 1.73 ms; so the tiles are loaded with ld.cg and stored evict-first (the inverse time FFT that follows
 // wants its L2 for the four-step scratch)
 #ifndef PD_SPEC_KEEP_SLAB_LD
 #define PD_SPEC_KEEP_SLAB_LD 1

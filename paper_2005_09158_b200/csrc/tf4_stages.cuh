@@ -51,7 +51,8 @@ PD_D void tf4_fwd_s1_tile(const double* __restrict__ r, long long S, long long p
           double x = 0.0, y = 0.0;
           if (VEC) {
             if (ok) {
-              const double2 u = __ldcs(reinterpret_cast<const double2*>(q + m * step));
+              // read once: ld.lu, 1.7 % faster than ld.cs on the cfg4 forward (r02aq); ld.cg loses 4 %
+              const double2 u = __ldlu(reinterpret_cast<const double2*>(q + m * step));
               x = u.x;
               y = u.y;
             }
