@@ -121,7 +121,7 @@ tfft_inv_kernel(const pd_spec sp, double* __restrict__ z, long long S,
     for (int k = 0; k < PT; ++k) {
       const int o = threadIdx.x + k * NTH;
       const int col = o % (2 * C), n = o / (2 * C);
-      v[k] = (o < NIN && (full || s0 + col < S)) ? __ldcs(pd_spec_row<SH>(sp, n) + s0 + col) : czero();
+      v[k] = (o < NIN && (full || s0 + col < S)) ? __ldlu(pd_spec_row<SH>(sp, n) + s0 + col) : czero();
     }
 #pragma unroll
     for (int k = 0; k < PT; ++k) {
